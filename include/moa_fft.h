@@ -1,0 +1,206 @@
+/*
+ * moa_fft.h -- C-ABI of the B200-native lifted FFT (libmoafft.so).
+ *
+ * The operation (PAPER.md, Mullin & Raynolds "Conformal Computing"):
+ * Van Loan's problem statement, "Input: x in C^n and n = 2^t, where t >= 0 is
+ * an integer.  Output: The FFT of x" (Fig. vanloan_fft), computed
+ * by dimension lifting: the vector is reshaped to a higher-rank array so that
+ * each block fits one level of the memory/processor hierarchy, and every pass
+ * is a reshape-transpose (Eq. reshape3), a block butterfly
+ * and a twiddle multiply with the transformed weights
+ * w_L^{sigma + j c^l}; the data is restored to natural order by
+ * the final transpose.  The lifting extends to the processor
+ * level.
+ *
+ * Semantics fixed by BASELINE.json: forward, unnormalised,
+ *     out[b*n + k] = sum_{j<n} in[b*n + j] * exp(-2 pi i j k / n),
+ * natural order in and out; for the 3-D plan the separable triple sum over a
+ * row-major [n0][n1][n2] array.  Elements are interleaved {re, im}:
+ * MOA_C64 = 2 x float32, MOA_C128 = 2 x float64.
+ *
+ * Conventions for every entry point:
+ *   - Return MOA_OK or an error code; a message is available from
+ *     moa_fft_last_error() (thread-local).  Nothing is clamped silently.
+ *   - Argument checks run before any allocation or CUDA call.
+ *   - Device pointers belong to the device current when the plan was created.
+ *   - Plans own their scratch, twiddle tables and (ngpu > 1) communicator; the
+ *     caller owns in/out.  A plan is not re-entrant: serialise exec calls on one
+ *     plan.  Different plans are independent.  Results are bitwise
+ *     deterministic for a fixed plan (no atomics).
+ */
+#ifndef MOA_FFT_H
+#define MOA_FFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MOA_OK = 0,
+    MOA_EINVAL = 1,       /* invalid argument (size, dtype, pointer, alignment) */
+    MOA_ENOMEM = 2,       /* device or host allocation failed */
+    MOA_ECUDA = 3,        /* a CUDA runtime call or kernel launch failed */
+    MOA_ENCCL = 4,        /* an NCCL call failed (the communicator is aborted) */
+    MOA_EUNSUPPORTED = 5  /* valid request this build does not implement */
+} moa_status_t;
+
+typedef enum { MOA_C64 = 0, MOA_C128 = 1 } moa_dtype_t;
+
+typedef struct moa_fft_plan_s *moa_fft_plan_t; /* opaque, library-owned */
+
+#define MOA_MAX_DIGITS 6
+#define MOA_MAX_PASSES 16
+
+/*
+ * moa_fft_plan -- plan `batch` independent forward transforms of length n.
+ *   n      : transform length, a power of two, n >= 1 (t >= 0; n = 1 is
+ *            the identity).  Otherwise MOA_EINVAL.
+ *   batch  : number of contiguous rows (row b at element offset b*n), >= 1.
+ *   dtype  : MOA_C64 or MOA_C128.
+ *   ngpu   : processors the single transform is partitioned over, in {1,2,4,8}.
+ *            ngpu > 1 requires moa_fft_dist_init() first, batch == 1 and
+ *            n >= ngpu^2 (else MOA_EUNSUPPORTED).  Rank g then passes its block
+ *            in = x[g n/p, (g+1) n/p) and receives out = X[g n/p, (g+1) n/p).
+ * The lifting n = R_0 R_1 ... is chosen by the planner; the environment
+ * variable MOA_FFT_LIFT="r0,r1,..." overrides it (the paper's run-time blocking
+ * size c; for ablations).  Allocates device scratch (one buffer of
+ * the local data size, only when the lifting has more than one pass) and the
+ * twiddle tables on the current device.
+ */
+moa_status_t moa_fft_plan(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu);
+
+/* moa_fft_plan_lift -- as moa_fft_plan(ngpu = 1) with an explicit lifting:
+ * radices[0..nrad) are powers of two whose product is n (each <= 4096). */
+moa_status_t moa_fft_plan_lift(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype,
+                               const int64_t *radices, int nrad);
+
+/*
+ * moa_fft_plan_3d -- the separable 3-D forward DFT of a row-major
+ * [n0][n1][n2] array (multi-dimensional FFT as 1-D FFTs along each axis,
+ * PAPER.md P:641 footnote).  Each n_i a power of two, 2 <= n_i <= 4096.
+ * ngpu > 1: slab decomposition; rank g passes x-slab planes
+ * j0 in [g n0/p, (g+1) n0/p) (row-major [j0_loc][j1][j2]) and receives the
+ * y-slab k1 in [g n1/p, (g+1) n1/p) (row-major [k0][k1_loc][k2]).
+ */
+moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
+                             int ngpu);
+
+/*
+ * moa_fft_exec -- run the plan on device buffers, stream-ordered on `stream`
+ * (a cudaStream_t of the plan's device; NULL = legacy default stream).
+ *   in  : device pointer, `local elements` complex values (n*batch at ngpu=1),
+ *         16-byte aligned.  Not modified unless in == out.
+ *   out : device pointer, same size, 16-byte aligned; in == out is allowed.
+ * Returns without a host synchronisation; buffers must stay valid until the
+ * stream passes the exec.  NULL or misaligned pointers -> MOA_EINVAL.
+ */
+moa_status_t moa_fft_exec(moa_fft_plan_t plan, const void *in, void *out, void *stream);
+
+/*
+ * moa_fft_exec_host -- end-to-end variant for HOST buffers: copies host_in to
+ * a plan-owned device buffer, executes, copies the result to host_out, and
+ * synchronises `stream` before returning.  host_in / host_out should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for full copy bandwidth; pageable memory
+ * works but is slower.  host_in == host_out is allowed.
+ */
+moa_status_t moa_fft_exec_host(moa_fft_plan_t plan, const void *host_in, void *host_out, void *stream);
+
+/* moa_fft_destroy -- release every resource of the plan (NULL is a no-op). */
+moa_status_t moa_fft_destroy(moa_fft_plan_t plan);
+
+/* Thread-local message describing the last error returned on this thread. */
+const char *moa_fft_last_error(void);
+
+/* Local element count of a plan (elements this rank passes to exec). */
+int64_t moa_fft_local_elems(moa_fft_plan_t plan);
+
+/* Number of kernel launches one exec issues (for launch accounting). */
+int moa_fft_launches_per_exec(moa_fft_plan_t plan);
+
+/*
+ * Processor-level lifting (ngpu > 1; SPMD, one process per GPU).
+ *   moa_fft_get_unique_id : rank 0 creates the 128-byte NCCL unique id; the
+ *                           caller broadcasts it (e.g. torch.distributed).
+ *   moa_fft_dist_init     : every rank, with the same id, before planning with
+ *                           ngpu > 1; binds the communicator to the current device.
+ *   moa_fft_dist_finalize : destroy the communicator.
+ */
+moa_status_t moa_fft_get_unique_id(uint8_t id[128]);
+moa_status_t moa_fft_dist_init(int rank, int ngpu, const uint8_t id[128]);
+moa_status_t moa_fft_dist_finalize(void);
+
+/*
+ * Loopback (one GPU, for tests): moa_fft_dist_loopback(rank, ngpu) makes the
+ * next ngpu > 1 plans on this thread belong to virtual rank `rank` (no
+ * communicator).  moa_fft_exec_loopback runs the ngpu plans (one per virtual
+ * rank, all on the current device) in lock step: the same kernels and chunk
+ * maps as the NCCL path, with every all-to-all done as device-to-device
+ * copies.  ins[r] / outs[r] are rank r's device buffers.
+ */
+moa_status_t moa_fft_dist_loopback(int rank, int ngpu);
+moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, const void *const *ins, void *const *outs,
+                                   void *stream);
+
+/*
+ * The distributed schedule of one rank (host only): passes[] as below; steps
+ * i < nsteps are kinds[i] = 0 (run passes[srcs[i]]) or 1 (all-to-all of
+ * counts[i] complex elements per peer from buffer srcs[i] to dsts[i]; buffer
+ * ids 0 in, 1 out, 2 scratch, 3 scratch2).  is3d = 0: n0 is the 1-D length.
+ */
+moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
+                               void *passes /* moa_pass_desc_t[max_passes] */, int max_passes, int *npasses,
+                               int32_t *kinds, int32_t *srcs, int32_t *dsts, int64_t *counts, int max_steps,
+                               int *nsteps);
+
+/*
+ * psi-index layer introspection (host only, no GPU needed).
+ *
+ * One pass = an ONF: for every line
+ * (digits d_0..d_{ndig-1}, d_i < ext[i], d_0 fastest) and every point k < R:
+ *   load  address = sum_i d_i*in_str[i]  + k*in_kstr    (elements)
+ *   store address = sum_i d_i*out_str[i] + k*out_kstr
+ *   the R-point DFT output k is multiplied by
+ *       w_{twN}^{(k * (tw_off + sum_i d_i*tw_str[i])) mod twN}   (twN <= 1: no twiddle)
+ *   and, when out_ksplit < logR, the store address of k is
+ *       sum_i d_i*out_str[i] + (k mod 2^out_ksplit)*out_kstr + (k >> out_ksplit)*out_kstr_hi.
+ * Consecutive lines of a tile (W of them) run along digit 0.
+ */
+typedef struct {
+    int32_t logR;               /* R = 2^logR points per line */
+    int32_t ndig;               /* number of line digits */
+    int64_t ext[MOA_MAX_DIGITS];
+    int64_t in_str[MOA_MAX_DIGITS];
+    int64_t out_str[MOA_MAX_DIGITS];
+    int64_t tw_str[MOA_MAX_DIGITS];
+    int64_t in_kstr, out_kstr;
+    int64_t twN;                /* twiddle root, power of two, or 1 */
+    int64_t tw_off;             /* added to the line's exponent base (rank offset; 0 on one GPU) */
+    int32_t out_ksplit;         /* store: k = khi*2^out_ksplit + klo, address += klo*out_kstr + khi*out_kstr_hi */
+    int64_t out_kstr_hi;
+    int32_t nodft;              /* 1: identity (a pure data-movement pass) */
+    int32_t lf_load, lf_store;  /* 1: that side is coalesced along the lines (digit 0) */
+    int32_t W;                  /* lines per CTA tile */
+    int32_t threads;            /* CTA size */
+    int32_t smem_bytes;         /* dynamic shared memory per CTA */
+    int32_t line_pad;           /* smem line stride = R + line_pad elements */
+    int32_t src, dst;           /* buffer ids: 0 = in, 1 = out, 2 = scratch, 3 = scratch2 */
+} moa_pass_desc_t;
+
+/* ONF descriptors of a 1-D lifting (radices == NULL: the planner's choice). */
+moa_status_t moa_psi_describe(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
+                              moa_pass_desc_t *out, int max_passes, int *npasses);
+/* ONF descriptors of the 3-D plan. */
+moa_status_t moa_psi_describe_3d(int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype, moa_pass_desc_t *out,
+                                 int max_passes, int *npasses);
+/* The planner's lifting for (n, batch, dtype) on one GPU. */
+moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64_t *radices, int max_rad,
+                              int *nrad);
+/* The descriptors a plan actually executes. */
+moa_status_t moa_fft_plan_describe(moa_fft_plan_t plan, moa_pass_desc_t *out, int max_passes, int *npasses);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOA_FFT_H */

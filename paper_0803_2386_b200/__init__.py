@@ -1,0 +1,299 @@
+"""paper_0803_2386_b200 -- Python binding of libmoafft.so (include/moa_fft.h).
+
+Argument marshalling only: every step of the FFT runs in the CUDA kernels of
+csrc/.  The names follow the C-ABI.  PyTorch is used by callers for device
+memory and streams; nothing here computes.  There is no CPU fallback: if the
+extension is missing, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libmoafft.so")
+
+MOA_OK, MOA_EINVAL, MOA_ENOMEM, MOA_ECUDA, MOA_ENCCL, MOA_EUNSUPPORTED = range(6)
+MOA_C64, MOA_C128 = 0, 1
+MAX_DIGITS = 6
+MAX_PASSES = 16
+STATUS_NAMES = {0: "MOA_OK", 1: "MOA_EINVAL", 2: "MOA_ENOMEM", 3: "MOA_ECUDA", 4: "MOA_ENCCL",
+                5: "MOA_EUNSUPPORTED"}
+
+# every symbol include/moa_fft.h declares
+EXPORTS = [
+    "moa_fft_plan", "moa_fft_plan_lift", "moa_fft_plan_3d", "moa_fft_exec", "moa_fft_exec_host",
+    "moa_fft_destroy", "moa_fft_last_error", "moa_fft_local_elems", "moa_fft_launches_per_exec",
+    "moa_fft_get_unique_id", "moa_fft_dist_init", "moa_fft_dist_finalize", "moa_fft_dist_loopback",
+    "moa_fft_exec_loopback", "moa_dist_describe", "moa_psi_describe", "moa_psi_describe_3d",
+    "moa_plan_radices", "moa_fft_plan_describe",
+]
+
+
+class PassDesc(ctypes.Structure):
+    """moa_pass_desc_t: one pass's ONF (see include/moa_fft.h)."""
+    _fields_ = [
+        ("logR", ctypes.c_int32), ("ndig", ctypes.c_int32),
+        ("ext", ctypes.c_int64 * MAX_DIGITS), ("in_str", ctypes.c_int64 * MAX_DIGITS),
+        ("out_str", ctypes.c_int64 * MAX_DIGITS), ("tw_str", ctypes.c_int64 * MAX_DIGITS),
+        ("in_kstr", ctypes.c_int64), ("out_kstr", ctypes.c_int64),
+        ("twN", ctypes.c_int64), ("tw_off", ctypes.c_int64),
+        ("out_ksplit", ctypes.c_int32), ("out_kstr_hi", ctypes.c_int64),
+        ("nodft", ctypes.c_int32),
+        ("lf_load", ctypes.c_int32), ("lf_store", ctypes.c_int32),
+        ("W", ctypes.c_int32), ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+        ("line_pad", ctypes.c_int32), ("src", ctypes.c_int32), ("dst", ctypes.c_int32),
+    ]
+
+    def to_dict(self) -> dict:
+        nd = self.ndig
+        return dict(logR=self.logR, R=1 << self.logR, ndig=nd, ext=list(self.ext[:nd]),
+                    in_str=list(self.in_str[:nd]), out_str=list(self.out_str[:nd]),
+                    tw_str=list(self.tw_str[:nd]), in_kstr=self.in_kstr, out_kstr=self.out_kstr,
+                    twN=self.twN, tw_off=self.tw_off, out_ksplit=self.out_ksplit,
+                    out_kstr_hi=self.out_kstr_hi, nodft=self.nodft, lf_load=self.lf_load,
+                    lf_store=self.lf_store, W=self.W, threads=self.threads,
+                    smem_bytes=self.smem_bytes, line_pad=self.line_pad, src=self.src, dst=self.dst)
+
+
+class MoaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} is missing: build it with __graft_entry__.build() "
+                          "(python -m paper_0803_2386_b200._build); there is no CPU fallback")
+    lib = ctypes.CDLL(_SO)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    P = ctypes.POINTER
+    sig = {
+        "moa_fft_plan": [P(vp), i64, i64, i32, i32],
+        "moa_fft_plan_lift": [P(vp), i64, i64, i32, P(i64), i32],
+        "moa_fft_plan_3d": [P(vp), i64, i64, i64, i32, i32],
+        "moa_fft_exec": [vp, vp, vp, vp],
+        "moa_fft_exec_host": [vp, vp, vp, vp],
+        "moa_fft_destroy": [vp],
+        "moa_fft_get_unique_id": [P(ctypes.c_uint8)],
+        "moa_fft_dist_init": [i32, i32, P(ctypes.c_uint8)],
+        "moa_fft_dist_finalize": [],
+        "moa_fft_dist_loopback": [i32, i32],
+        "moa_fft_exec_loopback": [P(vp), i32, P(vp), P(vp), vp],
+        "moa_dist_describe": [i32, i32, i32, i64, i64, i64, i32, vp, i32, P(i32), P(ctypes.c_int32),
+                              P(ctypes.c_int32), P(ctypes.c_int32), P(i64), i32, P(i32)],
+        "moa_psi_describe": [i64, i64, i32, P(i64), i32, P(PassDesc), i32, P(i32)],
+        "moa_psi_describe_3d": [i64, i64, i64, i32, P(PassDesc), i32, P(i32)],
+        "moa_plan_radices": [i64, i64, i32, P(i64), i32, P(i32)],
+        "moa_fft_plan_describe": [vp, P(PassDesc), i32, P(i32)],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.moa_fft_last_error.argtypes = []
+    lib.moa_fft_last_error.restype = ctypes.c_char_p
+    lib.moa_fft_local_elems.argtypes = [vp]
+    lib.moa_fft_local_elems.restype = i64
+    lib.moa_fft_launches_per_exec.argtypes = [vp]
+    lib.moa_fft_launches_per_exec.restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def _check(st: int):
+    if st != MOA_OK:
+        raise MoaError(st, lib.moa_fft_last_error().decode())
+
+
+def _dt(dtype) -> int:
+    if dtype in (MOA_C64, "c64", "complex64"):
+        return MOA_C64
+    if dtype in (MOA_C128, "c128", "complex128"):
+        return MOA_C128
+    if hasattr(dtype, "is_complex"):  # torch dtype
+        import torch
+        return MOA_C64 if dtype == torch.complex64 else MOA_C128
+    raise ValueError(f"unknown dtype {dtype!r}")
+
+
+# ---------------------------------------------------------------- C-ABI names
+def moa_fft_plan(n: int, batch: int = 1, dtype="c128", ngpu: int = 1) -> int:
+    h = ctypes.c_void_p()
+    _check(lib.moa_fft_plan(ctypes.byref(h), n, batch, _dt(dtype), ngpu))
+    return h.value
+
+
+def moa_fft_plan_lift(n: int, batch: int, dtype, radices) -> int:
+    h = ctypes.c_void_p()
+    arr = (ctypes.c_int64 * len(radices))(*radices)
+    _check(lib.moa_fft_plan_lift(ctypes.byref(h), n, batch, _dt(dtype), arr, len(radices)))
+    return h.value
+
+
+def moa_fft_plan_3d(n0: int, n1: int, n2: int, dtype="c128", ngpu: int = 1) -> int:
+    h = ctypes.c_void_p()
+    _check(lib.moa_fft_plan_3d(ctypes.byref(h), n0, n1, n2, _dt(dtype), ngpu))
+    return h.value
+
+
+def moa_fft_exec(plan: int, in_ptr: int, out_ptr: int, stream: int = 0) -> None:
+    _check(lib.moa_fft_exec(plan, in_ptr, out_ptr, stream))
+
+
+def moa_fft_exec_host(plan: int, in_ptr: int, out_ptr: int, stream: int = 0) -> None:
+    _check(lib.moa_fft_exec_host(plan, in_ptr, out_ptr, stream))
+
+
+def moa_fft_destroy(plan: int) -> None:
+    _check(lib.moa_fft_destroy(plan))
+
+
+def moa_fft_last_error() -> str:
+    return lib.moa_fft_last_error().decode()
+
+
+def moa_fft_local_elems(plan: int) -> int:
+    return int(lib.moa_fft_local_elems(plan))
+
+
+def moa_fft_launches_per_exec(plan: int) -> int:
+    return int(lib.moa_fft_launches_per_exec(plan))
+
+
+def moa_fft_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.moa_fft_get_unique_id(buf))
+    return bytes(buf)
+
+
+def moa_fft_dist_init(rank: int, ngpu: int, uid: bytes) -> None:
+    buf = (ctypes.c_uint8 * 128)(*uid)
+    _check(lib.moa_fft_dist_init(rank, ngpu, buf))
+
+
+def moa_fft_dist_finalize() -> None:
+    _check(lib.moa_fft_dist_finalize())
+
+
+def moa_fft_dist_loopback(rank: int, ngpu: int) -> None:
+    _check(lib.moa_fft_dist_loopback(rank, ngpu))
+
+
+def moa_fft_exec_loopback(plans, ins, outs, stream: int = 0) -> None:
+    p = len(plans)
+    _check(lib.moa_fft_exec_loopback((ctypes.c_void_p * p)(*plans), p, (ctypes.c_void_p * p)(*ins),
+                                     (ctypes.c_void_p * p)(*outs), stream))
+
+
+def moa_psi_describe(n: int, batch: int = 1, dtype="c128", radices=None) -> list:
+    out = (PassDesc * MAX_PASSES)()
+    np_ = ctypes.c_int()
+    arr = (ctypes.c_int64 * len(radices))(*radices) if radices else None
+    _check(lib.moa_psi_describe(n, batch, _dt(dtype), arr, len(radices) if radices else 0, out, MAX_PASSES,
+                                ctypes.byref(np_)))
+    return [out[i].to_dict() for i in range(np_.value)]
+
+
+def moa_psi_describe_3d(n0: int, n1: int, n2: int, dtype="c128") -> list:
+    out = (PassDesc * MAX_PASSES)()
+    np_ = ctypes.c_int()
+    _check(lib.moa_psi_describe_3d(n0, n1, n2, _dt(dtype), out, MAX_PASSES, ctypes.byref(np_)))
+    return [out[i].to_dict() for i in range(np_.value)]
+
+
+def moa_plan_radices(n: int, batch: int = 1, dtype="c128") -> list:
+    arr = (ctypes.c_int64 * 32)()
+    nr = ctypes.c_int()
+    _check(lib.moa_plan_radices(n, batch, _dt(dtype), arr, 32, ctypes.byref(nr)))
+    return list(arr[: nr.value])
+
+
+def moa_fft_plan_describe(plan: int) -> list:
+    out = (PassDesc * MAX_PASSES)()
+    np_ = ctypes.c_int()
+    _check(lib.moa_fft_plan_describe(plan, out, MAX_PASSES, ctypes.byref(np_)))
+    return [out[i].to_dict() for i in range(np_.value)]
+
+
+def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128") -> dict:
+    """Schedule of one rank: n = N (1-D) or (n0, n1, n2) (3-D slab)."""
+    is3d = isinstance(n, (tuple, list))
+    n0, n1, n2 = (n if is3d else (n, 0, 0))
+    passes = (PassDesc * MAX_PASSES)()
+    np_, ns = ctypes.c_int(), ctypes.c_int()
+    kinds, srcs, dsts = (ctypes.c_int32 * 32)(), (ctypes.c_int32 * 32)(), (ctypes.c_int32 * 32)()
+    counts = (ctypes.c_int64 * 32)()
+    _check(lib.moa_dist_describe(rank, ngpu, int(is3d), n0, n1, n2, _dt(dtype), ctypes.cast(passes, ctypes.c_void_p),
+                                 MAX_PASSES, ctypes.byref(np_), kinds, srcs, dsts, counts, 32, ctypes.byref(ns)))
+    steps = []
+    for i in range(ns.value):
+        if kinds[i] == 0:
+            steps.append(("pass", srcs[i]))
+        else:
+            steps.append(("alltoall", srcs[i], dsts[i], counts[i]))
+    return dict(passes=[passes[i].to_dict() for i in range(np_.value)], steps=steps)
+
+
+# ---------------------------------------------------------------- convenience
+class FFTPlan:
+    """RAII wrapper: FFTPlan(n, batch, dtype) or FFTPlan.plan_3d(...); exec on
+    torch device tensors (complex64 / complex128, contiguous)."""
+
+    def __init__(self, n: int = 0, batch: int = 1, dtype="c128", ngpu: int = 1, radices=None, _handle=None):
+        if _handle is not None:
+            self.h = _handle
+        elif radices is not None:
+            self.h = moa_fft_plan_lift(n, batch, dtype, radices)
+        else:
+            self.h = moa_fft_plan(n, batch, dtype, ngpu)
+        self.dtype = _dt(dtype)
+
+    @classmethod
+    def plan_3d(cls, n0, n1, n2, dtype="c128", ngpu: int = 1):
+        return cls(_handle=moa_fft_plan_3d(n0, n1, n2, dtype, ngpu), dtype=dtype)
+
+    @property
+    def local_elems(self) -> int:
+        return moa_fft_local_elems(self.h)
+
+    @property
+    def launches(self) -> int:
+        return moa_fft_launches_per_exec(self.h)
+
+    def describe(self) -> list:
+        return moa_fft_plan_describe(self.h)
+
+    def exec(self, x, out=None, stream=None):
+        import torch
+        want = torch.complex64 if self.dtype == MOA_C64 else torch.complex128
+        if x.dtype != want or not x.is_cuda or not x.is_contiguous():
+            raise ValueError(f"exec: expected a contiguous CUDA {want} tensor")
+        if x.numel() != self.local_elems:
+            raise ValueError(f"exec: expected {self.local_elems} elements, got {x.numel()}")
+        if out is None:
+            out = torch.empty_like(x)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        moa_fft_exec(self.h, x.data_ptr(), out.data_ptr(), s.cuda_stream)
+        return out
+
+    def exec_host(self, x_host, out_host, stream=None):
+        """End-to-end: host (pinned) buffers in and out; synchronises."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        moa_fft_exec_host(self.h, x_host.data_ptr(), out_host.data_ptr(), s.cuda_stream)
+        return out_host
+
+    def close(self):
+        if getattr(self, "h", None):
+            moa_fft_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,433 @@
+// abi.cpp -- the C-ABI (include/moa_fft.h): validation, plans, twiddle tables,
+// execution.  Every compute step runs in kernels.cu; this file only plans,
+// allocates and launches.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "moa_internal.h"
+
+namespace moa {
+
+static thread_local std::string g_err;
+
+moa_status_t fail(moa_status_t st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+static moa_status_t cuda_fail(cudaError_t e, const char *what) {
+    return fail(MOA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace moa
+
+using namespace moa;
+
+struct moa_fft_plan_s {
+    int device = -1;
+    moa_dtype_t dtype = MOA_C128;
+    int ngpu = 1;
+    int rank = 0;
+    bool is3d = false;
+    int64_t n = 0, batch = 1, n0 = 0, n1 = 0, n2 = 0;
+    int64_t local_elems = 0;
+    size_t esize = 16;
+    std::vector<moa_pass_desc_t> passes;
+    std::vector<DevTables> tabs;
+    std::vector<void *> allocs;
+    void *scratch = nullptr;
+    void *staging = nullptr;
+    DistPlan *dist = nullptr;  // processor-level lifting (comm.cpp)
+};
+
+namespace {
+
+bool pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+
+moa_status_t dev_alloc(moa_fft_plan_s *p, size_t bytes, void **out) {
+    *out = nullptr;
+    if (bytes == 0) return MOA_OK;
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOA_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+    p->allocs.push_back(*out);
+    return MOA_OK;
+}
+
+// w_N^e = e^{-2 pi i e / N} for exact integer e (forward sign), long double.
+void omega_ld(int64_t e, int64_t N, long double &re, long double &im) {
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    const long double a = two_pi * ((long double)e / (long double)N);
+    re = cosl(a);
+    im = -sinl(a);
+}
+
+moa_status_t upload_table(moa_fft_plan_s *p, const std::vector<long double> &v, const void **dptr) {
+    const size_t cnt = v.size();
+    void *d = nullptr;
+    moa_status_t st = dev_alloc(p, cnt * (p->dtype == MOA_C128 ? sizeof(double) : sizeof(float)), &d);
+    if (st) return st;
+    cudaError_t e;
+    if (p->dtype == MOA_C128) {
+        std::vector<double> h(cnt);
+        for (size_t i = 0; i < cnt; i++) h[i] = (double)v[i];
+        e = cudaMemcpy(d, h.data(), cnt * sizeof(double), cudaMemcpyHostToDevice);
+    } else {
+        std::vector<float> h(cnt);
+        for (size_t i = 0; i < cnt; i++) h[i] = (float)v[i];
+        e = cudaMemcpy(d, h.data(), cnt * sizeof(float), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "twiddle upload");
+    *dptr = d;
+    return MOA_OK;
+}
+
+// Plan-time twiddle tables (step a5): per pass the in-line table w_R^e (e < R)
+// and, for a lifted level, the two-level table of w_N (hi: w_N^{eh 2^h},
+// lo: w_N^{el}, h = ceil(log2 N / 2)).
+moa_status_t build_tables(moa_fft_plan_s *p) {
+    std::map<int, const void *> byR;
+    std::map<int64_t, std::pair<const void *, const void *>> byN;
+    p->tabs.clear();
+    for (auto &d : p->passes) {
+        DevTables t;
+        auto it = byR.find(d.logR);
+        if (it != byR.end()) {
+            t.twR = it->second;
+        } else {
+            const int64_t R = int64_t(1) << d.logR;
+            std::vector<long double> v(2 * R);
+            for (int64_t e = 0; e < R; e++) omega_ld(e, R, v[2 * e], v[2 * e + 1]);
+            moa_status_t st = upload_table(p, v, &t.twR);
+            if (st) return st;
+            byR[d.logR] = t.twR;
+        }
+        if (d.twN > 1) {
+            auto jt = byN.find(d.twN);
+            if (jt != byN.end()) {
+                t.tw_hi = jt->second.first;
+                t.tw_lo = jt->second.second;
+            } else {
+                const int lN = log2_exact(d.twN);
+                const int h = (lN + 1) / 2;
+                const int64_t nlo = int64_t(1) << h, nhi = d.twN >> h;
+                std::vector<long double> lo(2 * nlo), hi(2 * nhi);
+                for (int64_t e = 0; e < nlo; e++) omega_ld(e, d.twN, lo[2 * e], lo[2 * e + 1]);
+                for (int64_t e = 0; e < nhi; e++) omega_ld(e << h, d.twN, hi[2 * e], hi[2 * e + 1]);
+                moa_status_t st = upload_table(p, hi, &t.tw_hi);
+                if (st) return st;
+                st = upload_table(p, lo, &t.tw_lo);
+                if (st) return st;
+                byN[d.twN] = {t.tw_hi, t.tw_lo};
+            }
+        }
+        p->tabs.push_back(t);
+    }
+    return MOA_OK;
+}
+
+moa_status_t parse_lift_env(int64_t n, std::vector<int64_t> &rad, bool &have) {
+    have = false;
+    const char *s = std::getenv("MOA_FFT_LIFT");
+    if (!s || !*s) return MOA_OK;
+    rad.clear();
+    const char *c = s;
+    while (*c) {
+        char *end = nullptr;
+        long long v = std::strtoll(c, &end, 10);
+        if (end == c) return fail(MOA_EINVAL, "MOA_FFT_LIFT: expected comma-separated radices");
+        rad.push_back(v);
+        c = end;
+        if (*c == ',') c++;
+    }
+    int64_t prod = 1;
+    for (auto r : rad) prod *= r;
+    if (prod != n) return MOA_OK;  // the override applies only to the size it names
+    have = true;
+    return MOA_OK;
+}
+
+moa_status_t finish_plan(moa_fft_plan_s *p) {
+    cudaError_t e = cudaGetDevice(&p->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    for (auto &d : p->passes) {
+        int mt = 0, regs = 0;
+        e = kernel_attributes(p->dtype, d.logR, &mt, &regs);
+        if (e != cudaSuccess) return cuda_fail(e, "kernel attributes (is the GPU an sm_100 part?)");
+        if (d.threads > mt) return fail(MOA_EUNSUPPORTED, "pass tile exceeds the kernel's thread limit");
+    }
+    bool need_scratch = false;
+    for (auto &d : p->passes) need_scratch |= (d.src == 2 || d.dst == 2);
+    if (need_scratch) {
+        moa_status_t st = dev_alloc(p, size_t(p->local_elems) * p->esize, &p->scratch);
+        if (st) return st;
+    }
+    return build_tables(p);
+}
+
+moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,
+                     const int64_t *radices, int nrad) {
+    if (!plan) return fail(MOA_EINVAL, "plan: null output pointer");
+    *plan = nullptr;
+    if (!pow2(n)) return fail(MOA_EINVAL, "plan: n must be a power of two >= 1 (n = 2^t, t >= 0)");
+    if (batch < 1) return fail(MOA_EINVAL, "plan: batch must be >= 1");
+    if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan: unknown dtype");
+    if (!(ngpu == 1 || ngpu == 2 || ngpu == 4 || ngpu == 8)) return fail(MOA_EINVAL, "plan: ngpu must be 1, 2, 4 or 8");
+    if (n > (int64_t(1) << 36) || batch > (int64_t(1) << 36) / n)
+        return fail(MOA_EINVAL, "plan: n * batch exceeds 2^36 elements");
+    if (ngpu > 1) {
+        if (batch != 1) return fail(MOA_EUNSUPPORTED, "plan: ngpu > 1 requires batch == 1");
+        if (n < int64_t(ngpu) * ngpu) return fail(MOA_EUNSUPPORTED, "plan: ngpu > 1 requires n >= ngpu^2");
+        if (!dist_ready(ngpu)) return fail(MOA_EINVAL, "plan: call moa_fft_dist_init(rank, ngpu, id) first");
+    }
+    auto *p = new moa_fft_plan_s;
+    p->dtype = dtype;
+    p->n = n;
+    p->batch = batch;
+    p->ngpu = ngpu;
+    p->esize = dtype == MOA_C128 ? 16 : 8;
+    p->local_elems = n * batch / ngpu;
+    moa_status_t st = MOA_OK;
+    if (ngpu > 1) {
+        st = dist_plan_1d(p->dist, n, dtype);
+        if (!st) {
+            p->passes = p->dist->passes;
+            p->rank = p->dist->rank;
+        }
+    } else {
+        std::vector<int64_t> rad;
+        if (radices) {
+            rad.assign(radices, radices + nrad);
+        } else {
+            bool have = false;
+            st = parse_lift_env(n, rad, have);
+            if (!st && !have) st = plan_radices(n, batch, dtype, rad);
+        }
+        if (!st) st = psi_lift_passes(n, batch, dtype, rad.data(), int(rad.size()), p->passes);
+    }
+    if (!st) st = finish_plan(p);
+    if (st) {
+        std::string msg = moa_fft_last_error();
+        moa_fft_destroy(p);
+        return fail(st, msg);
+    }
+    *plan = p;
+    return MOA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *moa_fft_last_error(void) { return g_err.c_str(); }
+
+moa_status_t moa_fft_plan(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu) {
+    return plan_1d(plan, n, batch, dtype, ngpu, nullptr, 0);
+}
+
+moa_status_t moa_fft_plan_lift(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype,
+                               const int64_t *radices, int nrad) {
+    if (!radices || nrad < 1) return fail(MOA_EINVAL, "plan_lift: radices must be non-null with nrad >= 1");
+    return plan_1d(plan, n, batch, dtype, 1, radices, nrad);
+}
+
+moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype, int ngpu) {
+    if (!plan) return fail(MOA_EINVAL, "plan_3d: null output pointer");
+    *plan = nullptr;
+    for (int64_t v : {n0, n1, n2})
+        if (!pow2(v) || v > 4096) return fail(MOA_EINVAL, "plan_3d: each extent must be a power of two in [1, 4096]");
+    if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan_3d: unknown dtype");
+    if (!(ngpu == 1 || ngpu == 2 || ngpu == 4 || ngpu == 8)) return fail(MOA_EINVAL, "plan_3d: ngpu must be 1, 2, 4 or 8");
+    if (n0 * n1 * n2 > (int64_t(1) << 36)) return fail(MOA_EINVAL, "plan_3d: volume exceeds 2^36 elements");
+    if (ngpu > 1) {
+        if (n0 % ngpu || n1 % ngpu) return fail(MOA_EUNSUPPORTED, "plan_3d: ngpu must divide n0 and n1");
+        if (!dist_ready(ngpu)) return fail(MOA_EINVAL, "plan_3d: call moa_fft_dist_init(rank, ngpu, id) first");
+    }
+    auto *p = new moa_fft_plan_s;
+    p->dtype = dtype;
+    p->is3d = true;
+    p->n0 = n0;
+    p->n1 = n1;
+    p->n2 = n2;
+    p->n = n0 * n1 * n2;
+    p->ngpu = ngpu;
+    p->esize = dtype == MOA_C128 ? 16 : 8;
+    p->local_elems = p->n / ngpu;
+    moa_status_t st;
+    if (ngpu > 1) {
+        st = dist_plan_3d(p->dist, n0, n1, n2, dtype);
+        if (!st) {
+            p->passes = p->dist->passes;
+            p->rank = p->dist->rank;
+        }
+    } else {
+        st = psi_3d_passes(n0, n1, n2, 1, dtype, p->passes);
+    }
+    if (!st) st = finish_plan(p);
+    if (st) {
+        std::string msg = moa_fft_last_error();
+        moa_fft_destroy(p);
+        return fail(st, msg);
+    }
+    *plan = p;
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *stream) {
+    if (!p) return fail(MOA_EINVAL, "exec: null plan");
+    if (!in || !out) return fail(MOA_EINVAL, "exec: null buffer");
+    if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+        return fail(MOA_EINVAL, "exec: buffers must be 16-byte aligned");
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != p->device) return fail(MOA_EINVAL, "exec: the current device is not the plan's device");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (p->dist) return dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s);
+    for (size_t i = 0; i < p->passes.size(); i++) {
+        const moa_pass_desc_t &d = p->passes[i];
+        const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
+        void *dst = d.dst == 1 ? out : p->scratch;
+        e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
+        if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+    }
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host_out, void *stream) {
+    if (!p) return fail(MOA_EINVAL, "exec_host: null plan");
+    if (!host_in || !host_out) return fail(MOA_EINVAL, "exec_host: null buffer");
+    const size_t bytes = size_t(p->local_elems) * p->esize;
+    if (!p->staging) {
+        moa_status_t st = dev_alloc(p, bytes, &p->staging);
+        if (st) return st;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(p->staging, host_in, bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "exec_host H2D");
+    moa_status_t st = moa_fft_exec(p, p->staging, p->staging, stream);
+    if (st) return st;
+    e = cudaMemcpyAsync(host_out, p->staging, bytes, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "exec_host D2H");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "exec_host sync");
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_destroy(moa_fft_plan_t p) {
+    if (!p) return MOA_OK;
+    for (void *a : p->allocs) cudaFree(a);
+    if (p->dist) dist_plan_free(p->dist);
+    delete p;
+    return MOA_OK;
+}
+
+int64_t moa_fft_local_elems(moa_fft_plan_t p) { return p ? p->local_elems : -1; }
+
+int moa_fft_launches_per_exec(moa_fft_plan_t p) {
+    if (!p) return -1;
+    return p->dist ? dist_launches(p->dist, p->passes) : int(p->passes.size());
+}
+
+moa_status_t moa_psi_describe(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
+                              moa_pass_desc_t *out, int max_passes, int *npasses) {
+    if (!out || !npasses) return fail(MOA_EINVAL, "describe: null output");
+    if (!pow2(n) || batch < 1) return fail(MOA_EINVAL, "describe: n must be a power of two, batch >= 1");
+    if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "describe: unknown dtype");
+    std::vector<int64_t> rad;
+    moa_status_t st = MOA_OK;
+    if (radices) rad.assign(radices, radices + nrad);
+    else st = plan_radices(n, batch, dtype, rad);
+    if (st) return st;
+    std::vector<moa_pass_desc_t> v;
+    st = psi_lift_passes(n, batch, dtype, rad.data(), int(rad.size()), v);
+    if (st) return st;
+    if (int(v.size()) > max_passes) return fail(MOA_EINVAL, "describe: output array too small");
+    for (size_t i = 0; i < v.size(); i++) out[i] = v[i];
+    *npasses = int(v.size());
+    return MOA_OK;
+}
+
+moa_status_t moa_psi_describe_3d(int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype, moa_pass_desc_t *out,
+                                 int max_passes, int *npasses) {
+    if (!out || !npasses) return fail(MOA_EINVAL, "describe_3d: null output");
+    std::vector<moa_pass_desc_t> v;
+    moa_status_t st = psi_3d_passes(n0, n1, n2, 1, dtype, v);
+    if (st) return st;
+    if (int(v.size()) > max_passes) return fail(MOA_EINVAL, "describe_3d: output array too small");
+    for (size_t i = 0; i < v.size(); i++) out[i] = v[i];
+    *npasses = int(v.size());
+    return MOA_OK;
+}
+
+moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64_t *radices, int max_rad, int *nrad) {
+    if (!radices || !nrad) return fail(MOA_EINVAL, "plan_radices: null output");
+    std::vector<int64_t> r;
+    moa_status_t st = plan_radices(n, batch, dtype, r);
+    if (st) return st;
+    if (int(r.size()) > max_rad) return fail(MOA_EINVAL, "plan_radices: output array too small");
+    for (size_t i = 0; i < r.size(); i++) radices[i] = r[i];
+    *nrad = int(r.size());
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_plan_describe(moa_fft_plan_t p, moa_pass_desc_t *out, int max_passes, int *npasses) {
+    if (!p || !out || !npasses) return fail(MOA_EINVAL, "plan_describe: null argument");
+    if (int(p->passes.size()) > max_passes) return fail(MOA_EINVAL, "plan_describe: output array too small");
+    for (size_t i = 0; i < p->passes.size(); i++) out[i] = p->passes[i];
+    *npasses = int(p->passes.size());
+    return MOA_OK;
+}
+
+}  // extern "C"
+
+extern "C" moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, const void *const *ins,
+                                              void *const *outs, void *stream) {
+    if (!plans || !ins || !outs) return fail(MOA_EINVAL, "exec_loopback: null argument");
+    for (int r = 0; r < ngpu; r++) {
+        if (!plans[r] || !plans[r]->dist || !plans[r]->dist->loopback || plans[r]->dist->ngpu != ngpu ||
+            plans[r]->dist->rank != r)
+            return fail(MOA_EINVAL, "exec_loopback: plans[r] must be loopback plan of virtual rank r");
+        if (!ins[r] || !outs[r]) return fail(MOA_EINVAL, "exec_loopback: null buffer");
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto bufs = [&](int r, int id) -> void * {
+        moa_fft_plan_s *p = plans[r];
+        switch (id) {
+            case 0: return const_cast<void *>(ins[r]);
+            case 1: return outs[r];
+            case 2: return p->scratch;
+            default: return p->dist->scratch2;
+        }
+    };
+    const auto &steps = plans[0]->dist->steps;
+    for (const auto &st : steps) {
+        if (st.kind == 0) {
+            for (int r = 0; r < ngpu; r++) {
+                const moa_pass_desc_t &d = plans[r]->passes[st.pass];
+                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, d.dst), plans[r]->tabs[st.pass], s);
+                if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback pass: ") + cudaGetErrorString(e));
+            }
+        } else {
+            const size_t cb = size_t(st.count) * plans[0]->esize;
+            for (int h = 0; h < ngpu; h++)
+                for (int g = 0; g < ngpu; g++) {
+                    char *dst = static_cast<char *>(bufs(h, st.dst)) + size_t(g) * cb;
+                    const char *src = static_cast<const char *>(bufs(g, st.src)) + size_t(h) * cb;
+                    cudaError_t e = cudaMemcpyAsync(dst, src, cb, cudaMemcpyDeviceToDevice, s);
+                    if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback copy: ") + cudaGetErrorString(e));
+                }
+        }
+    }
+    return MOA_OK;
+}

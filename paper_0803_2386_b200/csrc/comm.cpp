@@ -1,0 +1,361 @@
+// comm.cpp -- processor-level lifting over NCCL (step a8).
+//
+// Schedules (verified on the host by tests/test_dist_gloo.py):
+//
+// 1-D, N = p M, rank g holds x[g M, (g+1) M) and receives X[g M, (g+1) M):
+//   X[k1 + p k2] = sum_{j_lo} w_M^{j_lo k2} w_N^{j_lo k1} sum_g x[g M + j_lo] w_p^{g k1}
+//   E1  all-to-all (chunk h of every block -> rank h)
+//   A   p-point DFT over g + lifted weight w_N^{(h M/p + m') k1}, stored [k1][m']
+//   E2  all-to-all (rank k1 now holds y[k1][j_lo] for all j_lo, natural order)
+//   B   the length-M lifted FFT of the local row (the one-GPU passes)
+//   E3  all-to-all (rank g' receives X'[k1][k2_loc], k2 in block g')
+//   U   p-way interleave out[k2_loc p + k1] (a data-movement pass)
+// 3-D slab, rank g holds planes j0 in [g n0/p, (g+1) n0/p):
+//   z-pass, y-pass stored in packed order [h][j0_loc][k1_loc][k2], one
+//   all-to-all, x-pass -> y-slab [k0][k1_loc][k2].
+//
+// NCCL is loaded at run time (dlopen of the libnccl.so.2 torch already loaded),
+// so the library itself loads on machines without it.
+#include <dlfcn.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "comm.h"
+#include "nccl.h"
+
+namespace moa {
+namespace {
+
+struct Nccl {
+    void *h = nullptr;
+    decltype(&::ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&::ncclCommInitRank) commInitRank = nullptr;
+    decltype(&::ncclCommDestroy) commDestroy = nullptr;
+    decltype(&::ncclCommAbort) commAbort = nullptr;
+    decltype(&::ncclAlltoAll) alltoAll = nullptr;
+    decltype(&::ncclGetErrorString) errStr = nullptr;
+};
+Nccl g_nccl;
+ncclComm_t g_comm = nullptr;
+int g_rank = -1, g_ngpu = 0;
+bool g_loopback = false;
+
+moa_status_t load_nccl() {
+    if (g_nccl.h) return MOA_OK;
+    const char *cand[] = {std::getenv("MOA_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    void *h = nullptr;
+    for (const char *c : cand)
+        if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return fail(MOA_ENCCL, "NCCL: cannot dlopen libnccl.so.2 (set MOA_NCCL_LIB)");
+    g_nccl.h = h;
+    g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.commAbort = (decltype(g_nccl.commAbort))dlsym(h, "ncclCommAbort");
+    g_nccl.alltoAll = (decltype(g_nccl.alltoAll))dlsym(h, "ncclAlltoAll");
+    g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.alltoAll)
+        return fail(MOA_ENCCL, "NCCL: the loaded library lacks ncclAlltoAll (needs NCCL >= 2.28)");
+    return MOA_OK;
+}
+
+moa_status_t nccl_fail(ncclResult_t r, const char *what) {
+    std::string m = std::string("NCCL ") + what + ": " + (g_nccl.errStr ? g_nccl.errStr(r) : "error");
+    if (g_comm && g_nccl.commAbort) {
+        g_nccl.commAbort(g_comm);
+        g_comm = nullptr;
+        g_rank = -1;
+        g_ngpu = 0;
+    }
+    return fail(MOA_ENCCL, m);
+}
+
+void dinit(moa_pass_desc_t &d, int logR) {
+    std::memset(&d, 0, sizeof(d));
+    d.logR = logR;
+    d.twN = 1;
+    d.out_ksplit = 62;
+}
+void dig(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, int64_t ts) {
+    if (ext == 1) return;
+    d.ext[d.ndig] = ext;
+    d.in_str[d.ndig] = is;
+    d.out_str[d.ndig] = os;
+    d.tw_str[d.ndig] = ts;
+    d.ndig++;
+}
+
+}  // namespace
+
+bool dist_ready(int ngpu) { return (g_comm || g_loopback) && g_ngpu == ngpu; }
+
+moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::vector<moa_pass_desc_t> &passes,
+                              std::vector<DistStep> &steps) {
+    passes.clear();
+    steps.clear();
+    const int64_t M = N / p, C = M / p;
+    const int lp = log2_exact(p);
+    // E1
+    steps.push_back({1, -1, 0, 2, C});
+    // A: p-point DFT over the received chunks, weights w_N^{(g C + m') k1}
+    {
+        moa_pass_desc_t d;
+        dinit(d, lp);
+        dig(d, C, 1, 1, 1);
+        d.in_kstr = d.out_kstr = C;
+        d.twN = N;
+        d.tw_off = int64_t(g) * C;
+        d.lf_load = d.lf_store = 1;
+        d.src = d.dst = 2;
+        psi_choose_tile(d, dtype);
+        steps.push_back({0, int(passes.size()), 2, 2, 0});
+        passes.push_back(d);
+    }
+    // E2
+    steps.push_back({1, -1, 2, 3, C});
+    // B: the local length-M FFT; buffer ids remapped in -> 3, scratch -> out(1), out -> 2
+    {
+        std::vector<int64_t> rad;
+        moa_status_t st = plan_radices(M, 1, dtype, rad);
+        if (st) return st;
+        std::vector<moa_pass_desc_t> b;
+        st = psi_lift_passes(M, 1, dtype, rad.data(), int(rad.size()), b);
+        if (st) return st;
+        const int remap[3] = {3, 2, 1};
+        for (auto &d : b) {
+            d.src = remap[d.src];
+            d.dst = remap[d.dst];
+            steps.push_back({0, int(passes.size()), d.src, d.dst, 0});
+            passes.push_back(d);
+        }
+    }
+    // E3
+    steps.push_back({1, -1, 2, 3, C});
+    // U: out[k2_loc p + k1] = buf[k1][k2_loc]
+    {
+        moa_pass_desc_t d;
+        dinit(d, lp);
+        dig(d, C, 1, p, 0);
+        d.in_kstr = C;
+        d.out_kstr = 1;
+        d.nodft = 1;
+        d.lf_load = 1;
+        d.lf_store = 0;
+        d.src = 3;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        steps.push_back({0, int(passes.size()), 3, 1, 0});
+        passes.push_back(d);
+    }
+    return MOA_OK;
+}
+
+moa_status_t dist_schedule_3d(int g, int p, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
+                              std::vector<moa_pass_desc_t> &passes, std::vector<DistStep> &steps) {
+    (void)g;
+    passes.clear();
+    steps.clear();
+    const int64_t n0l = n0 / p, n1l = n1 / p;
+    {  // z-pass on the x-slab
+        moa_pass_desc_t d;
+        dinit(d, log2_exact(n2));
+        dig(d, n1, n2, n2, 0);
+        dig(d, n0l, n1 * n2, n1 * n2, 0);
+        d.in_kstr = d.out_kstr = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        steps.push_back({0, int(passes.size()), 0, 1, 0});
+        passes.push_back(d);
+    }
+    {  // y-pass, stored in packed (send) order [h][j0_loc][k1_loc][k2]
+        moa_pass_desc_t d;
+        dinit(d, log2_exact(n1));
+        dig(d, n2, 1, 1, 0);
+        dig(d, n0l, n1 * n2, n1l * n2, 0);
+        d.in_kstr = n2;
+        d.out_kstr = n2;
+        d.out_ksplit = log2_exact(n1l);
+        d.out_kstr_hi = n0l * n1l * n2;
+        d.lf_load = d.lf_store = 1;
+        d.src = 1;
+        d.dst = 2;
+        psi_choose_tile(d, dtype);
+        steps.push_back({0, int(passes.size()), 1, 2, 0});
+        passes.push_back(d);
+    }
+    steps.push_back({1, -1, 2, 1, n0l * n1l * n2});
+    {  // x-pass on [n0][n1_loc][n2]
+        moa_pass_desc_t d;
+        dinit(d, log2_exact(n0));
+        dig(d, n2, 1, 1, 0);
+        dig(d, n1l, n2, n2, 0);
+        d.in_kstr = d.out_kstr = n1l * n2;
+        d.lf_load = d.lf_store = 1;
+        d.src = 1;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        steps.push_back({0, int(passes.size()), 1, 1, 0});
+        passes.push_back(d);
+    }
+    return MOA_OK;
+}
+
+moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype) {
+    dp = new DistPlan;
+    dp->rank = g_rank;
+    dp->ngpu = g_ngpu;
+    dp->loopback = g_loopback;
+    dp->esize = dtype == MOA_C128 ? 16 : 8;
+    dp->local_elems = n / g_ngpu;
+    moa_status_t st = dist_schedule_1d(g_rank, g_ngpu, n, dtype, dp->passes, dp->steps);
+    if (st) return st;
+    cudaError_t e = cudaMalloc(&dp->scratch2, size_t(dp->local_elems) * dp->esize);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        dp->scratch2 = nullptr;
+        return fail(MOA_ENOMEM, "dist: scratch allocation failed");
+    }
+    return MOA_OK;
+}
+
+moa_status_t dist_plan_3d(DistPlan *&dp, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype) {
+    dp = new DistPlan;
+    dp->rank = g_rank;
+    dp->ngpu = g_ngpu;
+    dp->loopback = g_loopback;
+    dp->esize = dtype == MOA_C128 ? 16 : 8;
+    dp->local_elems = n0 * n1 * n2 / g_ngpu;
+    return dist_schedule_3d(g_rank, g_ngpu, n0, n1, n2, dtype, dp->passes, dp->steps);
+}
+
+void dist_plan_free(DistPlan *dp) {
+    if (!dp) return;
+    if (dp->scratch2) cudaFree(dp->scratch2);
+    delete dp;
+}
+
+int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes) {
+    (void)passes;
+    int c = 0;
+    for (auto &s : dp->steps) c += s.kind == 0;
+    return c;
+}
+
+moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
+                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s) {
+    if (dp->loopback) return fail(MOA_EINVAL, "dist: a loopback plan runs through moa_fft_exec_loopback");
+    if (!g_comm) return fail(MOA_EINVAL, "dist: no communicator (moa_fft_dist_init)");
+    void *bufs[4] = {const_cast<void *>(in), out, scratch, dp->scratch2};
+    for (auto &st : dp->steps) {
+        if (st.kind == 0) {
+            const moa_pass_desc_t &d = passes[st.pass];
+            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[d.dst], tabs[st.pass], s);
+            if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("dist pass: ") + cudaGetErrorString(e));
+        } else {
+            const size_t cnt = size_t(st.count) * 2;
+            ncclResult_t r = g_nccl.alltoAll(bufs[st.src], bufs[st.dst], cnt, dtype == MOA_C128 ? ncclDouble : ncclFloat,
+                                             g_comm, s);
+            if (r != ncclSuccess) return nccl_fail(r, "all-to-all");
+        }
+    }
+    return MOA_OK;
+}
+
+}  // namespace moa
+
+using namespace moa;
+
+extern "C" {
+
+moa_status_t moa_fft_get_unique_id(uint8_t id[128]) {
+    if (!id) return fail(MOA_EINVAL, "get_unique_id: null output");
+    moa_status_t st = load_nccl();
+    if (st) return st;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    ncclUniqueId u;
+    ncclResult_t r = g_nccl.getUniqueId(&u);
+    if (r != ncclSuccess) return nccl_fail(r, "get unique id");
+    std::memcpy(id, &u, 128);
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_dist_init(int rank, int ngpu, const uint8_t id[128]) {
+    if (!id) return fail(MOA_EINVAL, "dist_init: null id");
+    if (!(ngpu == 2 || ngpu == 4 || ngpu == 8)) return fail(MOA_EINVAL, "dist_init: ngpu must be 2, 4 or 8");
+    if (rank < 0 || rank >= ngpu) return fail(MOA_EINVAL, "dist_init: rank out of range");
+    moa_status_t st = load_nccl();
+    if (st) return st;
+    if (g_comm) return fail(MOA_EINVAL, "dist_init: already initialised (moa_fft_dist_finalize first)");
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclComm_t c = nullptr;
+    ncclResult_t r = g_nccl.commInitRank(&c, ngpu, u, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "comm init");
+    g_comm = c;
+    g_rank = rank;
+    g_ngpu = ngpu;
+    g_loopback = false;
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_dist_finalize(void) {
+    if (g_comm) g_nccl.commDestroy(g_comm);
+    g_comm = nullptr;
+    g_rank = -1;
+    g_ngpu = 0;
+    g_loopback = false;
+    return MOA_OK;
+}
+
+// Loopback: plan virtual rank `rank` of `ngpu` on the current device with no
+// communicator; the plans of all virtual ranks execute together through
+// moa_fft_exec_loopback (exchanges become device-to-device copies).  Runs the
+// exact per-rank kernels and chunk maps of the NCCL path on one GPU.
+moa_status_t moa_fft_dist_loopback(int rank, int ngpu) {
+    if (!(ngpu == 2 || ngpu == 4 || ngpu == 8) || rank < 0 || rank >= ngpu)
+        return fail(MOA_EINVAL, "dist_loopback: bad rank / ngpu");
+    if (g_comm) return fail(MOA_EINVAL, "dist_loopback: a real communicator is active");
+    g_loopback = true;
+    g_rank = rank;
+    g_ngpu = ngpu;
+    return MOA_OK;
+}
+
+// Host-only: the distributed schedule of one rank (tests / introspection).
+// kinds[i] = 0 pass / 1 all-to-all; counts[i] = per-peer elements of an all-to-all.
+moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
+                               void *passes_v, int max_passes, int *npasses, int32_t *kinds,
+                               int32_t *srcs, int32_t *dsts, int64_t *counts, int max_steps, int *nsteps) {
+    moa_pass_desc_t *passes = static_cast<moa_pass_desc_t *>(passes_v);
+    if (!passes || !npasses || !kinds || !srcs || !dsts || !counts || !nsteps)
+        return fail(MOA_EINVAL, "dist_describe: null output");
+    if (!(ngpu == 2 || ngpu == 4 || ngpu == 8) || rank < 0 || rank >= ngpu)
+        return fail(MOA_EINVAL, "dist_describe: bad rank / ngpu");
+    std::vector<moa_pass_desc_t> ps;
+    std::vector<DistStep> ss;
+    moa_status_t st;
+    if (is3d) {
+        if (n0 % ngpu || n1 % ngpu) return fail(MOA_EUNSUPPORTED, "dist_describe: ngpu must divide n0, n1");
+        st = dist_schedule_3d(rank, ngpu, n0, n1, n2, dtype, ps, ss);
+    } else {
+        if (log2_exact(n0) < 0 || n0 < int64_t(ngpu) * ngpu) return fail(MOA_EUNSUPPORTED, "dist_describe: bad n");
+        st = dist_schedule_1d(rank, ngpu, n0, dtype, ps, ss);
+    }
+    if (st) return st;
+    if (int(ps.size()) > max_passes || int(ss.size()) > max_steps) return fail(MOA_EINVAL, "dist_describe: arrays too small");
+    for (size_t i = 0; i < ps.size(); i++) passes[i] = ps[i];
+    for (size_t i = 0; i < ss.size(); i++) {
+        kinds[i] = ss[i].kind;
+        srcs[i] = ss[i].kind == 0 ? ss[i].pass : ss[i].src;
+        dsts[i] = ss[i].dst;
+        counts[i] = ss[i].count;
+    }
+    *npasses = int(ps.size());
+    *nsteps = int(ss.size());
+    return MOA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,363 @@
+// kernels.cu -- sm_100a pass kernel of the lifted FFT (steps a3-a7 of
+// SURVEY.md §8(a)).
+//
+// One launch = one pass of the lifting.  A CTA owns a tile of W
+// adjacent lines of R = 2^LOG_R points.  Per tile:
+//   1. load   -- 128-bit vectorised global loads.  A pass whose points are
+//                strided (the reshape-transpose view, Eq. reshape3)
+//                loads W adjacent lines per point so each warp request covers
+//                whole 128-byte lines ("line-fast"), then transposes through
+//                shared memory; a pass with contiguous lines loads directly into
+//                registers ("point-fast").
+//   2. block butterflies -- the R-point DFT of every line as a sequence of
+//                Stockham steps of radix Q <= 16 done in registers (an in-register
+//                radix-2 network, FMA-shaped), with the step twiddles of a
+//                self-sorting (autosort) schedule.  The paper's input bit reversal
+//                P_n is never materialised: each step's output index map
+//                absorbs it (step a3).  Exchanges between steps go through
+//                XOR-swizzled shared memory (conflict-free for the access
+//                patterns used; see psi_choose_tile for the line padding).
+//   3. twiddle -- the lifted weights w_N^{(j k) mod N} from a
+//                two-level table (exact integer exponent; two table reads and one
+//                complex multiply), fused before the store.
+//   4. store  -- point-fast, or line-fast through shared memory (the final
+//                transpose F / digit reversal) with 128-byte runs.
+// No tensor cores: the FFT is not a dense contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <array>
+#include <type_traits>
+#include <utility>
+
+#include "moa_internal.h"
+
+namespace moa {
+namespace {
+
+// ---------------------------------------------------------------- complex ops
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
+    return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+    return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
+}
+template <typename V> struct RealOf;
+template <> struct RealOf<double2> { using type = double; };
+template <> struct RealOf<float2> { using type = float; };
+template <typename V> __device__ __forceinline__ V mk(typename RealOf<V>::type x, typename RealOf<V>::type y) {
+    V v;
+    v.x = x;
+    v.y = y;
+    return v;
+}
+
+// z * w_16^e for a compile-time e in [0, 8) (w_16 = e^{-2 pi i/16}); the
+// trivial and 1/sqrt2 cases are special-cased so no multiply by 0 or 1 is issued.
+template <int E, typename V> __device__ __forceinline__ V rot16(V z) {
+    using T = typename RealOf<V>::type;
+    constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173, H = 0.70710678118654752440;
+    if constexpr (E == 0) return z;
+    else if constexpr (E == 4) return mk<V>(z.y, -z.x);                          // * (-i)
+    else if constexpr (E == 2) return mk<V>((z.x + z.y) * T(H), (z.y - z.x) * T(H));   // * (1-i)/sqrt2
+    else if constexpr (E == 6) return mk<V>((z.y - z.x) * T(H), -(z.x + z.y) * T(H));  // * (-1-i)/sqrt2
+    else {
+        constexpr double wr = E == 1 ? C1 : E == 3 ? S1 : E == 5 ? -S1 : -C1;
+        constexpr double wi = E == 1 ? -S1 : E == 3 ? -C1 : E == 5 ? -C1 : -S1;
+        return cmul(z, mk<V>(T(wr), T(wi)));
+    }
+}
+
+// In-register DFT of Q = 2^LQ points, natural order in and out:
+// radix-2 decimation in frequency (span h = Q/2 ... 1, butterfly
+// (a, b) -> (a + b, (a - b) w_{2h}^i), cf. B_L of Fig. vanloan_fft
+// run backwards), then the compile-time bit-reversal of the register indices.
+template <int LQ> __device__ __forceinline__ constexpr int brev(int k) {
+    int r = 0;
+    for (int b = 0; b < LQ; b++)
+        if (k & (1 << b)) r |= 1 << (LQ - 1 - b);
+    return r;
+}
+template <int LQ, int H, int G, int I, typename V> __device__ __forceinline__ void dif_bfly(V *v) {
+    V a = v[G + I], b = v[G + I + H];
+    v[G + I] = cadd(a, b);
+    v[G + I + H] = rot16<I *(8 / H)>(csub(a, b));
+}
+template <int LQ, int H, typename V, int... Is> __device__ __forceinline__ void dif_span(V *v, std::integer_sequence<int, Is...>) {
+    // Is enumerates (group, i) pairs: g = (idx / H) * 2H, i = idx % H
+    (dif_bfly<LQ, H, (Is / H) * 2 * H, Is % H>(v), ...);
+}
+template <int LQ, int H, typename V> __device__ __forceinline__ void dif_all(V *v) {
+    if constexpr (H >= 1) {
+        dif_span<LQ, H>(v, std::make_integer_sequence<int, (1 << LQ) / 2>{});
+        dif_all<LQ, H / 2>(v);
+    }
+}
+template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
+    constexpr int Q = 1 << LQ;
+    if constexpr (Q > 1) {
+        dif_all<LQ, Q / 2>(v);
+        V t[Q];
+#pragma unroll
+        for (int k = 0; k < Q; k++) t[k] = v[brev<LQ>(k)];
+#pragma unroll
+        for (int k = 0; k < Q; k++) v[k] = t[k];
+    }
+}
+
+// XOR swizzle inside a line: bank group = low LB bits, permuted by a Gray code
+// of the higher bits (conflict-free for the Stockham write patterns; checked
+// exhaustively on the host for R = 2^1..2^12).
+template <int LB> __device__ __forceinline__ int swz(int i) {
+    const int hi = i >> LB;
+    return i ^ ((hi ^ (hi >> 1)) & ((1 << LB) - 1));
+}
+
+struct KArgs {
+    const void *in;
+    void *out;
+    int64_t in_str[kMaxDigits], out_str[kMaxDigits], tw_str[kMaxDigits];
+    int32_t lext[kMaxDigits];  // log2 extents
+    int32_t ndig;
+    int64_t in_kstr, out_kstr;
+    const void *twR, *tw_hi, *tw_lo;
+    int64_t twmask;  // twN - 1 (0: no twiddle)
+    int64_t tw_off;  // exponent base offset (processor-level lifting)
+    int32_t twh;     // split bit of the two-level table
+    int32_t ksplit;  // store: k = khi 2^ksplit + klo
+    int64_t out_kstr_hi;
+    int32_t nodft;
+    int32_t W, LS;   // lines per tile, smem line stride (elements)
+    int32_t lf_load, lf_store;
+};
+
+__device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
+    io = 0;
+    oo = 0;
+    te = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxDigits; i++) {
+        if (i < a.ndig) {
+            const int64_t d = line & ((int64_t(1) << a.lext[i]) - 1);
+            line >>= a.lext[i];
+            io += d * a.in_str[i];
+            oo += d * a.out_str[i];
+            te += d * a.tw_str[i];
+        }
+    }
+}
+
+// store offset of DFT output k (the ONF's k loop, optionally split in two)
+__device__ __forceinline__ int64_t kaddr(const KArgs &a, int k) {
+    return int64_t(k & ((1 << a.ksplit) - 1)) * a.out_kstr + int64_t(k >> a.ksplit) * a.out_kstr_hi;
+}
+
+template <typename V> __device__ __forceinline__ V ld_stream(const V *p);
+template <> __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
+template <> __device__ __forceinline__ float2 ld_stream(const float2 *p) { return __ldcs(p); }
+template <typename V> __device__ __forceinline__ void st_stream(V *p, V v) { __stcs(p, v); }
+
+// One Stockham step of radix Q = 2^LQ on a line of R = 2^LR points held as
+// P = 2^LP registers per thread (thread t holds points t + m R/P).  NS = 2^LNS
+// is the product of the previous radices.  Group j (= t + u R/P) reads points
+// j + r R/Q, multiplies by w_{NS Q}^{(j mod NS) r}, transforms, and writes to
+// (j / NS) NS Q + (j mod NS) + r NS (the self-sorting index map).
+template <int LR, int LP, int LQ, int LNS, bool LAST, int LB, typename V>
+__device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int t, const V *__restrict__ twR) {
+    constexpr int R = 1 << LR, P = 1 << LP, Q = 1 << LQ, NS = 1 << LNS, G = P / Q;
+#pragma unroll
+    for (int u = 0; u < G; u++) {
+        const int j = t + u * (R / P);
+        V v[Q];
+#pragma unroll
+        for (int r = 0; r < Q; r++) v[r] = pts[u + r * G];
+        if constexpr (NS > 1) {
+            const int jm = j & (NS - 1);
+#pragma unroll
+            for (int r = 1; r < Q; r++) v[r] = cmul(v[r], __ldg(twR + ((jm * r) << (LR - LNS - LQ))));
+        }
+        dft_reg<LQ>(v);
+        if constexpr (!LAST) {
+            const int base = ((j >> LNS) << (LNS + LQ)) + (j & (NS - 1));
+#pragma unroll
+            for (int r = 0; r < Q; r++) sm_line[swz<LB>(base + r * NS)] = v[r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < Q; r++) pts[u + r * G] = v[r];
+        }
+    }
+}
+
+template <int LR, int LP, int LB, int S, int NSTEP, typename V>
+__device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm_line, int t, const V *__restrict__ twR) {
+    constexpr int LQ0 = LR - LP * (NSTEP - 1);  // the small radix goes first (no twiddles at NS = 1)
+    constexpr int R = 1 << LR, P = 1 << LP;
+    constexpr int LQ = S == 0 ? LQ0 : LP;
+    constexpr int LNS = S == 0 ? 0 : LQ0 + LP * (S - 1);
+    constexpr bool LAST = S == NSTEP - 1;
+    stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm_line, t, twR);
+    if constexpr (!LAST) {
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = sm_line[swz<LB>(t + m * (R / P))];
+        __syncthreads();
+        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm_line, t, twR);
+    }
+}
+
+template <typename V, int LR>
+__global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
+    constexpr int LP = LR < 4 ? LR : 4;
+    constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
+    constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
+    constexpr int NSTEP = LR == 0 ? 1 : (LR + LP - 1) / LP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V *sm = reinterpret_cast<V *>(smem_raw);
+    const V *__restrict__ in = reinterpret_cast<const V *>(a.in);
+    V *__restrict__ out = reinterpret_cast<V *>(a.out);
+    const V *__restrict__ twR = reinterpret_cast<const V *>(a.twR);
+
+    const int tid = threadIdx.x;
+    const int64_t line0 = int64_t(blockIdx.x) * a.W;
+    // point-fast mapping: (l, t) with lanes over t inside one line
+    const int l = tid / TPL, t = tid % TPL;
+    V *sm_line = sm + l * a.LS;
+    V pts[P];
+
+    // ---- 1. load
+    if (a.lf_load) {
+        // line-fast mapping: lanes over the W adjacent lines (coalesced runs)
+        const int l2 = tid % a.W, t2 = tid / a.W;
+        int64_t io, oo, te;
+        line_offsets(a, line0 + l2, io, oo, te);
+        V tmp[P];
+#pragma unroll
+        for (int m = 0; m < P; m++) tmp[m] = ld_stream(in + io + int64_t(t2 + m * TPL) * a.in_kstr);
+        V *sl2 = sm + l2 * a.LS;
+#pragma unroll
+        for (int m = 0; m < P; m++) sl2[swz<LB>(t2 + m * TPL)] = tmp[m];
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = sm_line[swz<LB>(t + m * TPL)];
+        __syncthreads();
+    } else {
+        int64_t io, oo, te;
+        line_offsets(a, line0 + l, io, oo, te);
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(t + m * TPL) * a.in_kstr);
+    }
+
+    // ---- 2. block butterflies (R-point DFT of every line)
+    if constexpr (LR > 0) {
+        if (!a.nodft) line_fft<LR, LP, LB, 0, NSTEP>(pts, sm_line, t, twR);
+    }
+
+    // ---- 3. lifted weights w_N^{(e k) mod N}
+    if (a.twmask) {
+        int64_t io, oo, te;
+        line_offsets(a, line0 + l, io, oo, te);
+        const V *__restrict__ hi = reinterpret_cast<const V *>(a.tw_hi);
+        const V *__restrict__ lo = reinterpret_cast<const V *>(a.tw_lo);
+        const int64_t lomask = (int64_t(1) << a.twh) - 1;
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+            const int64_t k = t + m * TPL;
+            const int64_t e = ((te + a.tw_off) * k) & a.twmask;
+            if (e) {
+                const V w = cmul(__ldg(hi + (e >> a.twh)), __ldg(lo + (e & lomask)));
+                pts[m] = cmul(pts[m], w);
+            }
+        }
+    }
+
+    // ---- 4. store
+    if (a.lf_store) {
+#pragma unroll
+        for (int m = 0; m < P; m++) sm_line[swz<LB>(t + m * TPL)] = pts[m];
+        __syncthreads();
+        const int l2 = tid % a.W, t2 = tid / a.W;
+        int64_t io, oo, te;
+        line_offsets(a, line0 + l2, io, oo, te);
+        const V *sl2 = sm + l2 * a.LS;
+#pragma unroll
+        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, t2 + m * TPL), sl2[swz<LB>(t2 + m * TPL)]);
+    } else {
+        int64_t io, oo, te;
+        line_offsets(a, line0 + l, io, oo, te);
+#pragma unroll
+        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, t + m * TPL), pts[m]);
+    }
+}
+
+template <typename V> using KFn = void (*)(const KArgs);
+
+template <typename V, int... Ls> constexpr auto make_table(std::integer_sequence<int, Ls...>) {
+    return std::array<KFn<V>, sizeof...(Ls)>{&pass_kernel<V, Ls>...};
+}
+const std::array<KFn<double2>, 13> kTab128 = make_table<double2>(std::make_integer_sequence<int, 13>{});
+const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
+
+template <typename V>
+cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
+                     const DevTables &tb, cudaStream_t stream) {
+    KArgs a{};
+    a.in = in;
+    a.out = out;
+    a.ndig = d.ndig;
+    int64_t nlines = 1;
+    for (int i = 0; i < d.ndig; i++) {
+        a.in_str[i] = d.in_str[i];
+        a.out_str[i] = d.out_str[i];
+        a.tw_str[i] = d.tw_str[i];
+        a.lext[i] = log2_exact(d.ext[i]);
+        nlines *= d.ext[i];
+    }
+    a.in_kstr = d.in_kstr;
+    a.out_kstr = d.out_kstr;
+    a.twR = tb.twR;
+    a.tw_hi = tb.tw_hi;
+    a.tw_lo = tb.tw_lo;
+    a.twmask = d.twN > 1 ? d.twN - 1 : 0;
+    const int lN = log2_exact(d.twN);
+    a.twh = (lN + 1) / 2;
+    a.tw_off = d.tw_off;
+    a.ksplit = d.out_ksplit < d.logR ? d.out_ksplit : 30;
+    a.out_kstr_hi = d.out_kstr_hi;
+    a.nodft = d.nodft;
+    a.W = d.W;
+    a.LS = (1 << d.logR) + d.line_pad;
+    a.lf_load = d.lf_load;
+    a.lf_store = d.lf_store;
+    KFn<V> fn = tab[d.logR];
+    if (d.smem_bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t tiles = nlines / d.W;
+    fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
+                        cudaStream_t stream) {
+    if (d.logR < 0 || d.logR > 12) return cudaErrorInvalidValue;
+    if (dtype == MOA_C128) return launch_t<double2>(kTab128, d, in, out, tab, stream);
+    return launch_t<float2>(kTab64, d, in, out, tab, stream);
+}
+
+cudaError_t kernel_attributes(moa_dtype_t dtype, int logR, int *max_threads, int *regs) {
+    cudaFuncAttributes at{};
+    cudaError_t e = dtype == MOA_C128 ? cudaFuncGetAttributes(&at, kTab128[logR]) : cudaFuncGetAttributes(&at, kTab64[logR]);
+    if (e == cudaSuccess) {
+        *max_threads = at.maxThreadsPerBlock;
+        *regs = at.numRegs;
+    }
+    return e;
+}
+
+}  // namespace moa

@@ -1,0 +1,234 @@
+// psi.cpp -- the psi-index layer (host): lifting shape -> ONF pass descriptors.
+//
+// PAPER.md grounding:
+//   * the reshape-transpose <r c> rho-hat (transpose (<r c> rho-hat x)) reduces
+//     to the two-loop ONF "for j < c, for i < r: @x + j + c*i" (Eq. trans
+//     P:2897-2923, Fig. loopindex): a loop nest of (extent, stride)
+//     pairs with an affine address -- exactly what moa_pass_desc_t stores;
+//   * the final transpose reduces to "for t < 2^{d-sigma}, s < 2^sigma:
+//     @x + s*2^{d-sigma} + t";
+//   * the psi Correspondence Theorem (Eq. psi_corr): a partial
+//     index selects a contiguous block, so a line's points are one affine
+//     stride and the inner loops of a tile are contiguous runs.
+// All sizes are powers of two, so every div/mod of the DNF becomes a shift or a
+// mask and is removed from the loops by restructuring them, as the paper does
+// for i' = int(c i / r), j' = (j + i c) mod r.
+//
+// Lifting: n = R_0 R_1 ... R_{P-1}.  Pass p < P-1 views the data
+// as <B_p R_p S_p> (S_p = R_{p+1}...R_{P-1}) and transforms along the middle
+// axis in place, multiplying output k of line (o, j) by w_{R_p S_p}^{j k} (the
+// transformed weights of the lifted level).  The last pass
+// transforms the contiguous rows and stores through the axis-reversing
+// transpose (the lifted final transpose), giving natural order.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "moa_internal.h"
+
+namespace moa {
+
+int log2_exact(int64_t n) {
+    if (n < 1) return -1;
+    int t = 0;
+    while ((int64_t(1) << t) < n) t++;
+    return (int64_t(1) << t) == n ? t : -1;
+}
+
+static void desc_init(moa_pass_desc_t &d, int logR) {
+    std::memset(&d, 0, sizeof(d));
+    d.logR = logR;
+    d.twN = 1;
+    d.out_ksplit = 62;  // no split
+}
+
+static void add_digit(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, int64_t ts) {
+    if (ext == 1) return;  // a loop of extent 1 contributes nothing to the ONF
+    d.ext[d.ndig] = ext;
+    d.in_str[d.ndig] = is;
+    d.out_str[d.ndig] = os;
+    d.tw_str[d.ndig] = ts;
+    d.ndig++;
+}
+
+void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
+    const int esize = dtype == MOA_C128 ? 16 : 8;
+    const int slots = 128 / esize;        // elements per 128-byte smem row / DRAM line
+    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int64_t R = int64_t(1) << logR, TPL = R >> logP;
+    const bool lf = d.lf_load || d.lf_store;
+    const int64_t ext0 = d.ndig ? d.ext[0] : 1;
+    // Lines per tile: enough adjacent lines for full 128-byte runs on a
+    // line-coalesced side; enough threads per CTA otherwise.
+    int64_t W = lf ? slots : (TPL >= 256 ? 1 : 256 / TPL);
+    const int64_t smem_cap = 100 * 1024;  // two CTAs per SM
+    while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
+    if (W < 1) W = 1;
+    d.W = int32_t(W);
+    d.threads = int32_t(W * TPL);
+    int64_t pad;
+    if (TPL >= slots) pad = lf ? (W >= slots ? 1 : slots / W) : 1;
+    else pad = TPL;
+    d.line_pad = int32_t(pad);
+    const bool needs_smem = lf || logR > logP;
+    d.smem_bytes = needs_smem ? int32_t(W * (R + pad) * esize) : 0;
+}
+
+moa_status_t psi_lift_passes(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
+                             std::vector<moa_pass_desc_t> &out) {
+    out.clear();
+    if (nrad < 1 || nrad > MOA_MAX_PASSES) return fail(MOA_EINVAL, "psi: lifting must have 1..16 factors");
+    int64_t prod = 1;
+    for (int i = 0; i < nrad; i++) {
+        int lr = log2_exact(radices[i]);
+        if (lr < 0 || lr > 12) return fail(MOA_EINVAL, "psi: each radix must be a power of two <= 4096");
+        prod *= radices[i];
+    }
+    if (prod != n) return fail(MOA_EINVAL, "psi: the radices must multiply to n");
+    if (nrad + 1 > MOA_MAX_DIGITS + 1) return fail(MOA_EUNSUPPORTED, "psi: too many passes");
+    const int P = nrad;
+    if (P == 1) {
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n));
+        add_digit(d, batch, n, n, 0);
+        d.in_kstr = d.out_kstr = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        return MOA_OK;
+    }
+    for (int p = 0; p < P - 1; p++) {
+        int64_t Sp = 1;
+        for (int q = p + 1; q < P; q++) Sp *= radices[q];
+        const int64_t Np = radices[p] * Sp, Op = batch * n / Np;
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(radices[p]));
+        add_digit(d, Sp, 1, 1, 1);    // j: the contiguous inner index, weight exponent j*k
+        add_digit(d, Op, Np, Np, 0);  // o: the rows above
+        d.in_kstr = d.out_kstr = Sp;
+        d.twN = Np;
+        d.lf_load = d.lf_store = 1;
+        d.src = p == 0 ? 0 : 2;
+        d.dst = 2;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+    }
+    {
+        const int64_t RL = radices[P - 1];
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(RL));
+        int64_t above = 1;  // R_0 ... R_{i-1}
+        for (int i = 0; i < P - 1; i++) {
+            const int64_t in_s = n / (above * radices[i]);  // n / (R_0 ... R_i)
+            add_digit(d, radices[i], in_s, above, 0);
+            above *= radices[i];
+        }
+        add_digit(d, batch, n, n, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n / RL;
+        d.lf_load = 0;
+        d.lf_store = 1;
+        d.src = 2;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+    }
+    return MOA_OK;
+}
+
+moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, moa_dtype_t dtype,
+                           std::vector<moa_pass_desc_t> &out) {
+    out.clear();
+    const int64_t ns[3] = {n0, n1, n2};
+    for (int a = 0; a < 3; a++) {
+        int l = log2_exact(ns[a]);
+        if (l < 0 || l > 12) return fail(MOA_EINVAL, "psi: 3-D extents must be powers of two <= 4096");
+    }
+    const int64_t plane = n1 * n2, vol = n0 * plane;
+    // axis 2: contiguous lines
+    {
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n2));
+        add_digit(d, n1, n2, n2, 0);
+        add_digit(d, n0, plane, plane, 0);
+        add_digit(d, howmany, vol, vol, 0);
+        d.in_kstr = d.out_kstr = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        if (n2 > 1) out.push_back(d);
+    }
+    // axis 1: lines along stride n2, tile over contiguous j2
+    {
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n1));
+        add_digit(d, n2, 1, 1, 0);
+        add_digit(d, n0, plane, plane, 0);
+        add_digit(d, howmany, vol, vol, 0);
+        d.in_kstr = d.out_kstr = n2;
+        d.lf_load = d.lf_store = 1;
+        d.src = out.empty() ? 0 : 1;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        if (n1 > 1) out.push_back(d);
+    }
+    // axis 0
+    {
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n0));
+        add_digit(d, n2, 1, 1, 0);
+        add_digit(d, n1, n2, n2, 0);
+        add_digit(d, howmany, vol, vol, 0);
+        d.in_kstr = d.out_kstr = plane;
+        d.lf_load = d.lf_store = 1;
+        d.src = out.empty() ? 0 : 1;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        if (n0 > 1) out.push_back(d);
+    }
+    if (out.empty()) {  // 1 x 1 x 1: identity copy as a 1-point pass
+        moa_pass_desc_t d;
+        desc_init(d, 0);
+        add_digit(d, howmany, 1, 1, 0);
+        d.in_kstr = d.out_kstr = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+    }
+    return MOA_OK;
+}
+
+// Planner (step a1): the fewest passes whose per-pass line fits one CTA tile,
+// radices as equal as possible (largest first) so every pass is one HBM round
+// trip of similar cost.  Per-CTA limit: 2^9 points for the line-coalesced
+// passes (8 adjacent lines x 2^9 x 16 B = 64 KiB), 2^12 for the last pass.
+moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vector<int64_t> &radices) {
+    (void)batch;
+    radices.clear();
+    const int t = log2_exact(n);
+    if (t < 0) return fail(MOA_EINVAL, "plan: n must be a power of two");
+    const int max_single = 12;                      // one pass holds 2^12 points per line
+    const int max_mid = dtype == MOA_C128 ? 9 : 10;  // strided passes: W adjacent lines per tile
+    if (t <= max_single) {
+        radices.push_back(n);
+        return MOA_OK;
+    }
+    // P passes: P-1 strided passes of <= max_mid bits plus a last pass <= max_single
+    int P = 2;
+    while ((P - 1) * max_mid + max_single < t) P++;
+    // distribute t bits: balanced, with the last pass taking the remainder
+    std::vector<int> bits(P, t / P);
+    for (int i = 0; i < t % P; i++) bits[P - 1 - i]++;
+    // respect the per-pass caps by moving bits to the last pass
+    for (int i = 0; i < P - 1; i++)
+        while (bits[i] > max_mid) {
+            bits[i]--;
+            bits[P - 1]++;
+        }
+    for (int b : bits) radices.push_back(int64_t(1) << b);
+    return MOA_OK;
+}
+
+}  // namespace moa

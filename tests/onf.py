@@ -1,0 +1,80 @@
+"""Test-side evaluation of the psi-layer's ONF descriptors, straight from the
+semantics documented in include/moa_fft.h (loops over the line digits, affine
+load / store addresses, twiddle exponent), plus a plain numpy executor of a
+pass list / distributed schedule.  Used only by tests."""
+import numpy as np
+
+
+def enumerate_pass(d):
+    """-> (load[line][k], store[line][k], tw_exp[line][k]) as int64 arrays, lines
+    in ONF order (digit 0 fastest)."""
+    R = d["R"]
+    ext = d["ext"]
+    nlines = int(np.prod(ext)) if ext else 1
+    line = np.arange(nlines, dtype=np.int64)
+    io = np.zeros(nlines, np.int64)
+    oo = np.zeros(nlines, np.int64)
+    te = np.zeros(nlines, np.int64)
+    rest = line.copy()
+    for e, si, so, st in zip(ext, d["in_str"], d["out_str"], d["tw_str"]):
+        dig = rest % e
+        rest //= e
+        io += dig * si
+        oo += dig * so
+        te += dig * st
+    k = np.arange(R, dtype=np.int64)
+    load = io[:, None] + k[None, :] * d["in_kstr"]
+    if d["out_ksplit"] < d["logR"]:
+        lo = k & ((1 << d["out_ksplit"]) - 1)
+        hi = k >> d["out_ksplit"]
+        koff = lo * d["out_kstr"] + hi * d["out_kstr_hi"]
+    else:
+        koff = k * d["out_kstr"]
+    store = oo[:, None] + koff[None, :]
+    if d["twN"] > 1:
+        tw = ((te[:, None] + d["tw_off"]) * k[None, :]) % d["twN"]
+    else:
+        tw = np.zeros_like(load)
+    return load, store, tw
+
+
+def run_pass(d, src, dst):
+    load, store, tw = enumerate_pass(d)
+    R = d["R"]
+    lines = src[load]
+    if not d["nodft"]:
+        F = np.exp(-2j * np.pi * np.outer(np.arange(R), np.arange(R)) / R)
+        lines = lines @ F.T
+    if d["twN"] > 1:
+        lines = lines * np.exp(-2j * np.pi * tw / d["twN"])
+    dst[store] = lines
+
+
+def run_plan(passes, x):
+    bufs = {0: x.astype(np.complex128).copy(), 1: np.zeros(x.size, np.complex128),
+            2: np.zeros(x.size, np.complex128), 3: np.zeros(x.size, np.complex128)}
+    for d in passes:
+        run_pass(d, bufs[d["src"]], bufs[d["dst"]])
+    return bufs[1]
+
+
+def run_dist(schedules, shards):
+    """schedules[r] = moa_dist_describe(r, p, ...); shards[r] = rank r's input."""
+    p = len(schedules)
+    m = shards[0].size
+    bufs = [{0: s.astype(np.complex128).copy(), 1: np.zeros(m, np.complex128), 2: np.zeros(m, np.complex128),
+             3: np.zeros(m, np.complex128)} for s in shards]
+    nsteps = len(schedules[0]["steps"])
+    for i in range(nsteps):
+        st = schedules[0]["steps"][i]
+        if st[0] == "pass":
+            for r in range(p):
+                d = schedules[r]["passes"][schedules[r]["steps"][i][1]]
+                run_pass(d, bufs[r][d["src"]], bufs[r][d["dst"]])
+        else:
+            _, s, t, c = st
+            snap = [bufs[g][s].copy() for g in range(p)]
+            for h in range(p):
+                for g in range(p):
+                    bufs[h][t][g * c:(g + 1) * c] = snap[g][h * c:(h + 1) * c]
+    return [b[1] for b in bufs]

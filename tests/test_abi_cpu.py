@@ -1,0 +1,148 @@
+"""The C-ABI library on the CPU: it loads, exports every symbol include/moa_fft.h
+declares, rejects bad arguments before touching CUDA, and its psi-index layer
+emits ONF descriptors that are bit-exact against the oracle's MoA-materialised
+maps.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import moa
+from onf import enumerate_pass, run_dist, run_plan
+
+import paper_0803_2386_b200 as m
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "moa_fft.h")).read()
+    declared = set(re.findall(r"^\s*(?:moa_status_t|const char \*|int64_t|int)\s*\*?\s*(moa_\w+)\s*\(", hdr, re.M))
+    assert declared, "no declarations parsed"
+    assert declared == set(m.EXPORTS), declared ^ set(m.EXPORTS)
+    so = ctypes.CDLL(m._SO)
+    for name in declared:
+        assert hasattr(so, name), name
+
+
+@pytest.mark.parametrize("args,status", [
+    ((0, 1, "c128", 1), m.MOA_EINVAL), ((12, 1, "c128", 1), m.MOA_EINVAL), ((-4, 1, "c128", 1), m.MOA_EINVAL),
+    ((1024, 0, "c128", 1), m.MOA_EINVAL), ((1024, 1, "c128", 3), m.MOA_EINVAL),
+    ((1024, 1, "c128", 16), m.MOA_EINVAL), ((1024, 2, "c128", 2), m.MOA_EUNSUPPORTED),
+    ((8, 1, "c128", 4), m.MOA_EUNSUPPORTED), ((1024, 1, "c128", 2), m.MOA_EINVAL),
+    ((1 << 40, 1, "c64", 1), m.MOA_EINVAL),
+])
+def test_plan_argument_errors(args, status):
+    with pytest.raises(m.MoaError) as ei:
+        m.moa_fft_plan(*args)
+    assert ei.value.status == status
+    assert m.moa_fft_last_error()
+
+
+def test_other_argument_errors():
+    h = ctypes.c_void_p()
+    assert m.lib.moa_fft_plan(ctypes.byref(h), 1024, 1, 7, 1) == m.MOA_EINVAL       # unknown dtype
+    assert m.lib.moa_fft_plan(None, 1024, 1, 1, 1) == m.MOA_EINVAL                    # null out
+    assert m.lib.moa_fft_exec(None, None, None, None) == m.MOA_EINVAL                 # null plan
+    with pytest.raises(m.MoaError):
+        m.moa_fft_plan_3d(1024, 1000, 8)
+    with pytest.raises(m.MoaError):
+        m.moa_fft_plan_3d(8192, 8, 8)
+    with pytest.raises(m.MoaError):
+        m.moa_fft_plan_lift(64, 1, "c128", [4, 4])                                      # product != n
+    with pytest.raises(m.MoaError):
+        m.moa_psi_describe(64, 1, "c128", [8, 3, 3])
+    assert m.lib.moa_fft_destroy(None) == m.MOA_OK
+
+
+def test_planner_liftings():
+    assert m.moa_plan_radices(1 << 10) == [1 << 10]
+    assert m.moa_plan_radices(1 << 16) == [256, 256]
+    r3 = m.moa_plan_radices(1 << 28, 1, "c128")
+    assert np.prod(r3) == 1 << 28 and len(r3) == 3 and max(r3[:-1]) <= 512
+    r4 = m.moa_plan_radices(1 << 30, 1, "c64")
+    assert np.prod(r4) == 1 << 30 and len(r4) == 3
+    for t in range(0, 34):
+        r = m.moa_plan_radices(1 << t)
+        assert int(np.prod(r)) == 1 << t and all(x <= 4096 for x in r)
+
+
+def _as_dict(load, store, tw):
+    return {tuple(a): (tuple(b), tuple(c)) for a, b, c in zip(load.tolist(), store.tolist(), tw.tolist())}
+
+
+@pytest.mark.parametrize("radices,batch", [([4, 8], 1), ([8, 8], 2), ([2, 4, 8], 1), ([4, 2, 2, 4], 3), ([16], 2),
+                                           ([8, 4, 16], 1), ([2, 2], 1), ([32, 16], 2), ([64], 1)])
+def test_psi_descriptors_bit_exact_vs_oracle_maps(radices, batch):
+    n = int(np.prod(radices))
+    got = m.moa_psi_describe(n, batch, "c128", radices)
+    ref = moa.lift_pass_maps(radices, batch)
+    assert len(got) == len(ref)
+    for d, r in zip(got, ref):
+        assert d["R"] == r["R"]
+        load, store, tw = enumerate_pass(d)
+        mine = _as_dict(load, store, tw if d["twN"] > 1 else np.zeros_like(tw))
+        theirs = _as_dict(np.array(r["load"]), np.array(r["store"]), np.array(r["tw"]))
+        assert mine == theirs
+        if d["twN"] > 1:
+            assert d["twN"] == r["twN"]
+        # every element is loaded once and stored once (a permutation per pass)
+        assert sorted(load.ravel().tolist()) == list(range(n * batch))
+        assert sorted(store.ravel().tolist()) == list(range(n * batch))
+
+
+@pytest.mark.parametrize("n,batch,dtype", [(1 << 12, 2, "c128"), (1 << 16, 1, "c128"), (1 << 13, 1, "c64"),
+                                           (1 << 20, 1, "c128"), (1 << 21, 1, "c64")])
+def test_planner_descriptors_compute_the_dft(n, batch, dtype):
+    # executing the planner's own ONF with plain numpy reproduces the oracle's DFT
+    passes = m.moa_psi_describe(n, batch, dtype)
+    x = synth.fill(n * batch, 5, synth.UNIFORM)
+    got = run_plan(passes, x)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+    for d in passes:                                    # tiles are legal
+        assert d["threads"] <= 512 and d["smem_bytes"] <= 100 * 1024
+        if d["ndig"]:
+            assert d["ext"][0] % d["W"] == 0
+
+
+def test_psi_3d_descriptors():
+    for shape in [(8, 4, 16), (16, 16, 16), (2, 32, 4)]:
+        passes = m.moa_psi_describe_3d(*shape)
+        x = synth.fill(int(np.prod(shape)), 6, synth.NORMAL)
+        got = run_plan(passes, x).reshape(shape)
+        ref = oracle.fft3d(x.reshape(shape))
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_1d_schedule_host_simulation(p):
+    # processor-level lifting: every rank's ONF + the all-to-all chunk maps reproduce the DFT
+    N = 1 << 12
+    x = synth.fill(N, 8, synth.UNIFORM)
+    sch = [m.moa_dist_describe(r, p, N, "c64") for r in range(p)]
+    kinds = [s[0] for s in sch[0]["steps"]]
+    assert kinds.count("alltoall") == 3
+    outs = run_dist(sch, np.split(x, p))
+    ref = oracle.fft_radix2(x)
+    got = np.concatenate(outs)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_3d_schedule_host_simulation(p):
+    shape = (16, 8, 4)
+    x = synth.fill(int(np.prod(shape)), 9, synth.NORMAL).reshape(shape)
+    sch = [m.moa_dist_describe(r, p, shape, "c128") for r in range(p)]
+    assert [s[0] for s in sch[0]["steps"]].count("alltoall") == 1
+    shards = [np.ascontiguousarray(s).reshape(-1) for s in np.split(x, p, axis=0)]
+    outs = run_dist(sch, shards)
+    ref = oracle.fft3d(x)
+    n1l = shape[1] // p
+    for r in range(p):
+        want = ref[:, r * n1l:(r + 1) * n1l, :].reshape(-1)       # y-slab [k0][k1_loc][k2]
+        assert np.linalg.norm(outs[r] - want) / np.linalg.norm(want) < 1e-12

@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path through the C-ABI against the oracle, on the same
+seeded inputs (synth/).  Tolerances are BASELINE.json's: relative L2 error
+<= 1e-11 (complex128) and <= 2e-5 (complex64)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-11, "c64": 2e-5}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def m(torch_cuda):
+    import paper_0803_2386_b200 as mod
+    return mod
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def gpu_run(torch, plan, x: np.ndarray, inplace=False):
+    xt = torch.from_numpy(x).cuda()
+    out = xt if inplace else torch.empty_like(xt)
+    plan.exec(xt, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def npdt(dtype):
+    return np.complex128 if dtype == "c128" else np.complex64
+
+
+# ---------------------------------------------------------------- cfg1
+def test_cfg1_vs_direct_dft(m, torch_cuda):
+    c = synth.CONFIGS["cfg1"]
+    x = synth.config_input("cfg1")
+    plan = m.FFTPlan(c["n"], 1, "c128")
+    y = gpu_run(torch_cuda, plan, x)
+    assert rel_l2(y, oracle.dft_direct(x)) <= 1e-11           # BASELINE.json: checked against O(n^2)
+    assert rel_l2(y, oracle.fft_radix2(x)) <= 1e-11
+
+
+# ---------------------------------------------------------------- sweeps
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("t", list(range(0, 23)))
+def test_sizes_sweep(m, torch_cuda, dtype, t):
+    n = 1 << t
+    batch = max(1, min(5, (1 << 20) // n)) if t < 20 else 1
+    x = synth.fill(n * batch, 1000 + t, synth.UNIFORM, dtype)
+    plan = m.FFTPlan(n, batch, dtype)
+    y = gpu_run(torch_cuda, plan, x)
+    ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+    assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype], (n, batch, plan.describe())
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("radices,batch", [
+    ([2, 2], 3), ([2, 2, 2, 2, 2], 1), ([4, 8], 7), ([16, 16], 2), ([8, 32, 4], 1), ([512, 512], 1),
+    ([4096, 2], 1), ([2, 4096], 1), ([64, 64, 64], 1), ([1024, 256], 1), ([128, 64, 16, 8], 1),
+    ([2048, 2048], 1), ([32, 4096], 1), ([4096, 16], 3),
+])
+def test_explicit_liftings(m, torch_cuda, dtype, radices, batch):
+    # the paper's run-time blocking choice, including unbalanced and
+    # all-radix-2 liftings (the unblocked-control extreme)
+    n = int(np.prod(radices))
+    x = synth.fill(n * batch, 7, synth.NORMAL, dtype)
+    plan = m.FFTPlan(n, batch, dtype, radices=radices)
+    y = gpu_run(torch_cuda, plan, x)
+    ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+    assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- edge cases
+def test_identity_and_tiny(m, torch_cuda):
+    for dtype in ("c128", "c64"):
+        x = synth.fill(37, 3, synth.UNIFORM, dtype)
+        y = gpu_run(torch_cuda, m.FFTPlan(1, 37, dtype), x)               # n = 1: identity (t = 0)
+        assert np.array_equal(y, x)
+        x = synth.fill(2 * 1001, 3, synth.UNIFORM, dtype)
+        y = gpu_run(torch_cuda, m.FFTPlan(2, 1001, dtype), x)
+        ref = np.stack([x[0::2] + x[1::2], x[0::2] - x[1::2]], axis=1).reshape(-1)
+        assert rel_l2(y, ref) <= TOL[dtype]
+
+
+def test_in_place_and_determinism(m, torch_cuda):
+    for n, batch in [(1 << 10, 4), (1 << 16, 3), (1 << 21, 1)]:
+        x = synth.fill(n * batch, 11, synth.UNIFORM)
+        plan = m.FFTPlan(n, batch, "c128")
+        y1 = gpu_run(torch_cuda, plan, x)
+        y2 = gpu_run(torch_cuda, plan, x, inplace=True)
+        y3 = gpu_run(torch_cuda, plan, x)
+        assert np.array_equal(y1, y2) and np.array_equal(y1, y3)      # bitwise deterministic, in-place ok
+
+
+def test_exec_rejects_bad_pointers(m, torch_cuda):
+    torch = torch_cuda
+    plan = m.FFTPlan(1024, 1, "c128")
+    buf = torch.empty(2048 + 1, dtype=torch.complex64, device="cuda")
+    with pytest.raises(m.MoaError) as ei:
+        m.moa_fft_exec(plan.h, buf.data_ptr() + 8, buf.data_ptr() + 8, 0)    # 8-byte aligned only
+    assert ei.value.status == m.MOA_EINVAL
+    with pytest.raises(m.MoaError):
+        m.moa_fft_exec(plan.h, 0, buf.data_ptr(), 0)
+
+
+def test_closed_forms_large(m, torch_cuda):
+    n = 1 << 22
+    d = np.zeros(n, np.complex128)
+    d[0] = 1
+    y = gpu_run(torch_cuda, m.FFTPlan(n, 1, "c128"), d)
+    assert np.max(np.abs(y - 1)) < 1e-12
+    k0 = 123457
+    j = np.arange(n)
+    e = np.exp(2j * np.pi * ((k0 * j) % n) / n)
+    y = gpu_run(torch_cuda, m.FFTPlan(n, 1, "c128"), e)
+    assert abs(y[k0] - n) < 1e-6
+    y[k0] = 0
+    assert np.max(np.abs(y)) < 1e-6
+
+
+def test_exec_host_e2e(m, torch_cuda):
+    torch = torch_cuda
+    n, batch = 1 << 14, 8
+    x = synth.fill(n * batch, 12, synth.UNIFORM)
+    plan = m.FFTPlan(n, batch, "c128")
+    hin = torch.from_numpy(x).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    plan.exec_host(hin, hout)
+    assert rel_l2(hout.numpy(), oracle.fft_radix2_rows(x, n)) <= 1e-11
+
+
+# ---------------------------------------------------------------- 3-D
+@pytest.mark.parametrize("shape", [(8, 8, 8), (4, 16, 32), (64, 32, 16), (2, 2, 2), (1, 8, 4), (128, 128, 128)])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_3d(m, torch_cuda, shape, dtype):
+    N = int(np.prod(shape))
+    x = synth.fill(N, 13, synth.NORMAL, dtype)
+    plan = m.FFTPlan.plan_3d(*shape, dtype=dtype)
+    y = gpu_run(torch_cuda, plan, x).reshape(shape)
+    ref = oracle.fft3d(x.astype(np.complex128).reshape(shape))
+    assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- loopback processor lifting
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_dist_1d_loopback(m, torch_cuda, p, dtype):
+    torch = torch_cuda
+    N = 1 << 20
+    x = synth.fill(N, 3, synth.UNIFORM, dtype)
+    plans = []
+    for r in range(p):
+        m.moa_fft_dist_loopback(r, p)
+        plans.append(m.FFTPlan(N, 1, dtype, ngpu=p))
+    shards = [torch.from_numpy(s.copy()).cuda() for s in np.split(x, p)]
+    outs = [torch.empty_like(s) for s in shards]
+    m.moa_fft_exec_loopback([pl.h for pl in plans], [s.data_ptr() for s in shards], [o.data_ptr() for o in outs],
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    y = np.concatenate([o.cpu().numpy() for o in outs]).astype(np.complex128)
+    ref = oracle.fft_radix2(x.astype(np.complex128))
+    assert rel_l2(y, ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_3d_loopback(m, torch_cuda, p):
+    torch = torch_cuda
+    shape = (64, 32, 16)
+    x = synth.fill(int(np.prod(shape)), 4, synth.NORMAL).reshape(shape)
+    plans = []
+    for r in range(p):
+        m.moa_fft_dist_loopback(r, p)
+        plans.append(m.FFTPlan.plan_3d(*shape, dtype="c128", ngpu=p))
+    shards = [torch.from_numpy(np.ascontiguousarray(s).reshape(-1)).cuda() for s in np.split(x, p, axis=0)]
+    outs = [torch.empty_like(s) for s in shards]
+    m.moa_fft_exec_loopback([pl.h for pl in plans], [s.data_ptr() for s in shards], [o.data_ptr() for o in outs],
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = oracle.fft3d(x)
+    n1l = shape[1] // p
+    for r in range(p):
+        want = ref[:, r * n1l:(r + 1) * n1l, :].reshape(-1)
+        assert rel_l2(outs[r].cpu().numpy(), want) <= 1e-11
+
+
+# ---------------------------------------------------------------- BASELINE.json full sizes
+def _sample_bins(n, count, seed):
+    rng = np.random.default_rng(seed)
+    fixed = [0, 1, n // 2, n - 1, n // 3]
+    return np.unique(np.concatenate([fixed, rng.integers(0, n, count)]).astype(np.int64))
+
+
+def test_cfg2_full(m, torch_cuda):
+    c = synth.CONFIGS["cfg2"]
+    n, b = c["n"], c["batch"]
+    x = synth.config_input("cfg2")
+    y = gpu_run(torch_cuda, m.FFTPlan(n, b, "c128"), x)
+    ref = oracle.fft_radix2_rows(x, n)                      # the whole 1 GiB against the oracle
+    assert rel_l2(y, ref) <= 1e-11
+
+
+@pytest.mark.slow
+def test_cfg3_full_sampled(m, torch_cuda):
+    n = synth.CONFIGS["cfg3"]["n"]
+    x = synth.config_input("cfg3")
+    y = gpu_run(torch_cuda, m.FFTPlan(n, 1, "c128"), x)
+    bins = _sample_bins(n, 6, 2)
+    ref = oracle.dft_bins(x, n, bins)
+    scale = np.sqrt(n) * np.sqrt(np.mean(np.abs(x) ** 2))    # |X[k]| ~ sqrt(n) rms(x)
+    assert np.max(np.abs(y[bins] - ref)) / scale <= 1e-11
+    # Parseval at full size
+    assert abs(np.vdot(y, y).real / (n * np.vdot(x, x).real) - 1) < 1e-12
+
+
+@pytest.mark.slow
+def test_cfg4_full_sampled(m, torch_cuda):
+    n = synth.CONFIGS["cfg4"]["n"]
+    x = synth.config_input("cfg4")
+    y = gpu_run(torch_cuda, m.FFTPlan(n, 1, "c64"), x)
+    bins = _sample_bins(n, 4, 3)
+    ref = oracle.dft_bins(x, n, bins)
+    scale = np.sqrt(n) * np.sqrt(np.mean(np.abs(x.astype(np.complex128)) ** 2))
+    assert np.max(np.abs(y[bins].astype(np.complex128) - ref)) / scale <= 2e-5
+    e_in = np.sum(np.abs(x.astype(np.complex128)) ** 2)
+    e_out = np.sum(np.abs(y.astype(np.complex128)) ** 2)
+    assert abs(e_out / (n * e_in) - 1) < 1e-5
+
+
+@pytest.mark.slow
+def test_cfg5_full_sampled(m, torch_cuda):
+    shape = synth.CONFIGS["cfg5"]["shape"]
+    x = synth.config_input("cfg5")
+    y = gpu_run(torch_cuda, m.FFTPlan.plan_3d(*shape, dtype="c128"), x)
+    rng = np.random.default_rng(4)
+    ks = np.array([(0, 0, 0), (1, 2, 3), (1023, 512, 7)] + [tuple(rng.integers(0, 1024, 3)) for _ in range(2)],
+                  dtype=np.int64)
+    ref = oracle.dft3_bins(x, shape, ks)
+    got = y.reshape(shape)[ks[:, 0], ks[:, 1], ks[:, 2]]
+    N = int(np.prod(shape))
+    scale = np.sqrt(N) * np.sqrt(np.mean(np.abs(x) ** 2))
+    assert np.max(np.abs(got - ref)) / scale <= 1e-11
+    assert abs(np.vdot(y, y).real / (N * np.vdot(x, x).real) - 1) < 1e-12
