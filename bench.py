@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""bench.py -- the hot path (the lifted FFT) timed on B200, plus the oracle.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfgX] [--impl reference]
+
+A "step" is one moa_fft_exec of the workload (every pass of the lifted FFT over
+one batch of synthetic input already resident in HBM).  Default workload is
+BASELINE.json configs[1] (cfg2: 1024 rows x 2^16 complex128).  One JSON line is
+printed by rank 0.  For N > 1 (torchrun, one process per GPU) cfg1-cfg3 run as
+independent per-rank replicas (weak scaling); cfg4 / cfg5 are partitioned over
+the ranks with NCCL all-to-alls (strong scaling).
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload on the host cores: the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FFT GFLOP/s (5n·log2n/t) and achieved HBM GB/s vs peak, at 1/2/4/8 B200"
+
+WORKLOADS = {
+    "cfg1": dict(desc="single 1D forward complex128 FFT, n=2^10, uniform, seed 0", n=1 << 10, batch=1,
+                 dtype="c128", kind="1d"),
+    "cfg2": dict(desc="batched 1D forward complex128 FFT, n=2^16, batch=1024 rows (1 GiB), uniform, seed 1",
+                 n=1 << 16, batch=1024, dtype="c128", kind="1d"),
+    "cfg3": dict(desc="single 1D forward complex128 FFT, n=2^28 (4 GiB), normal, seed 2", n=1 << 28, batch=1,
+                 dtype="c128", kind="1d"),
+    "cfg4": dict(desc="single 1D forward complex64 FFT, n=2^30 (8 GiB), uniform, seed 3", n=1 << 30, batch=1,
+                 dtype="c64", kind="1d", partitioned=True),
+    "cfg5": dict(desc="3D forward complex128 FFT 1024^3 (16 GiB), normal, seed 4", shape=(1024, 1024, 1024),
+                 dtype="c128", kind="3d", partitioned=True),
+}
+# HBM round trips (passes) of the algorithm per config
+ALG_PASSES = {"cfg1": 1, "cfg2": 1, "cfg3": 2, "cfg4": 2, "cfg5": 3}
+
+
+def flops_per_step(w, ranks_units=1):
+    if w["kind"] == "3d":
+        N = w["shape"][0] * w["shape"][1] * w["shape"][2]
+        return 5.0 * N * math.log2(N)
+    return 5.0 * w["n"] * math.log2(w["n"]) * w["batch"] * ranks_units
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def oracle_sample(wname, budget_s):
+    """Time the oracle (as it stands) on a bounded sample of the workload.
+    -> (GFLOP/s, sample description, threads)."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    w = WORKLOADS[wname]
+    thr = oracle.max_threads()
+    if wname in ("cfg1", "cfg2"):
+        n = w["n"]
+        rows_per_chunk = 4096 if n <= 1024 else 16
+        x = synth.fill(n * rows_per_chunk, synth.CONFIGS[wname]["seed"], synth.CONFIGS[wname]["dist"])
+        rows, t0 = 0, time.perf_counter()
+        while True:
+            a = x.copy()
+            oracle.fft_radix2_rows_inplace(a, n)
+            rows += rows_per_chunk
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
+        gf = 5.0 * n * math.log2(n) * rows / el / 1e9
+        return gf, f"{rows} rows of the {wname} workload (n={n}, complex128 radix-2 oracle O1+O2), {el:.1f} s", thr
+    # single huge transforms: one oracle transform of a scaled-down length of the same kind
+    if w["kind"] == "3d":
+        s = 256
+        x = synth.fill(s ** 3, 4, synth.NORMAL).reshape(s, s, s)
+        t0 = time.perf_counter()
+        oracle.fft3d_inplace(x)
+        el = time.perf_counter() - t0
+        N = s ** 3
+        return 5.0 * N * math.log2(N) / el / 1e9, f"one {s}^3 complex128 3-D oracle FFT (O5; cfg5 scaled 1/64), {el:.1f} s", thr
+    n = 1 << 24
+    x = synth.fill(n, synth.CONFIGS[wname]["seed"], synth.CONFIGS[wname]["dist"])
+    t0 = time.perf_counter()
+    oracle.fft_radix2_inplace(x)
+    el = time.perf_counter() - t0
+    return (5.0 * n * math.log2(n) / el / 1e9,
+            f"one 2^24-point complex128 radix-2 oracle FFT ({wname} length scaled down), {el:.1f} s", thr)
+
+
+def run_reference(args, w, rank):
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+
+    wname = args.workload
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        gf, sample, thr = oracle_sample(wname, budget_s=1.0)
+        if i >= args.warmup:
+            vals.append(gf)
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{wname}: {w['desc']}"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, w, rank)
+
+    import numpy as np
+    import torch
+
+    import paper_0803_2386_b200 as m
+    import synth
+
+    torch.cuda.set_device(local)
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+    partitioned = dist and w.get("partitioned", False)
+
+    # ---- plan
+    if partitioned:
+        uid = [m.moa_fft_get_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(uid, src=0)
+        m.moa_fft_dist_init(rank, world, uid[0])
+    t0 = time.perf_counter()
+    if w["kind"] == "3d":
+        plan = m.FFTPlan.plan_3d(*w["shape"], dtype=w["dtype"], ngpu=world if partitioned else 1)
+    else:
+        plan = m.FFTPlan(w["n"], w["batch"], w["dtype"], ngpu=world if partitioned else 1)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    L = plan.local_elems
+    esize = 16 if w["dtype"] == "c128" else 8
+    cfgsyn = synth.CONFIGS[args.workload]
+    e0 = rank * L if partitioned else 0
+    xh = synth.fill(L, cfgsyn["seed"], cfgsyn["dist"], w["dtype"], e0=e0)
+    x = torch.from_numpy(xh).cuda()
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    data_bytes = L * esize
+    small = data_bytes * 2 < 256 << 20
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if small else None
+
+    def barrier():
+        if dist:
+            td.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        plan.exec(x, y, stream)
+    barrier()
+
+    # ---- timed region (per-step events; per-pass events inside the library)
+    launches = plan.launches
+    m.moa_fft_prof_begin(plan.h, args.steps)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)] if small else None
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        if small:
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)                        # evict L2 between timed iterations
+                ev[2 * i].record(stream)
+                plan.exec(x, y, stream)
+                ev[2 * i + 1].record(stream)
+            barrier()
+            total_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps))
+        else:
+            start.record(stream)
+            for _ in range(args.steps):
+                plan.exec(x, y, stream)
+            end.record(stream)
+            barrier()
+            total_ms = start.elapsed_time(end)
+    step_ms_list, nexec = m.moa_fft_prof_end(plan.h)
+    ms = total_ms / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- throughput
+    units = world if (dist and not partitioned) else 1
+    flops = flops_per_step(w, units)
+    value = flops / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    desc = plan.describe()
+    kinds = []
+    if partitioned:
+        sched = m.moa_dist_describe(rank, world, w["shape"] if w["kind"] == "3d" else w["n"], w["dtype"])
+        kinds = [s[0] for s in sched["steps"]]
+    else:
+        kinds = ["pass"] * len(desc)
+    per_step = [s / max(nexec, 1) for s in step_ms_list]
+    pass_idx = [i for i, k in enumerate(kinds) if k == "pass"]
+    dom = max(pass_idx, key=lambda i: per_step[i])
+    dom_ms = per_step[dom]
+    dom_bytes = 2 * data_bytes                   # one HBM round trip of the local array per pass launch
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    alg_bytes = ALG_PASSES[args.workload] * 2 * data_bytes
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(args.workload, {}).get(str(dom))
+    except Exception:
+        pass
+    pdesc = desc[pass_idx.index(dom)] if not partitioned else sched["passes"][[s[1] for s in sched["steps"] if s[0] == "pass"][pass_idx.index(dom)]]
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4), "traffic": traffic,
+        "kernel": f"pass_kernel<{'double2' if w['dtype'] == 'c128' else 'float2'},{pdesc['logR']}> (step {dom})",
+        "kernel_ms": round(dom_ms, 4), "kernel_alg_bytes": dom_bytes, "peak_source": peak_src,
+        "step_alg_bytes": alg_bytes,
+        "step_frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peak, 4),
+        "per_step_ms": [round(v, 4) for v in per_step], "step_kinds": kinds,
+    }
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        hin = torch.from_numpy(xh).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        plan.exec_host(hin, hout, stream)
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.exec_host(hin, hout, stream)
+        s1.record(stream)
+        barrier()
+        ems = s0.elapsed_time(s1) / args.e2e_steps
+        if dist:
+            t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+            td.all_reduce(t, op=td.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(flops / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": data_bytes, "d2h_bytes_per_step": data_bytes, "ms_per_step": round(ems, 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gf, sample, thr = oracle_sample(args.workload, budget_s=12.0)
+        cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        cfg = {"workload": f"{args.workload}: {w['desc']}", "dtype_elem": w["dtype"],
+               "lifting": [d["R"] for d in desc] if w["kind"] == "1d" and not partitioned else None,
+               "passes": len(desc), "plan_ms": round(plan_ms, 1),
+               "l2": "L2 flushed (512 MiB write) before every timed iteration" if small else
+               f"inputs larger than L2 ({data_bytes / 2**30:.2f} GiB in + out per rank)",
+               "parallelism": (f"processor-lifted over {world} ranks (NCCL all-to-all)" if partitioned else
+                               (f"{world} independent replicas" if dist else "1 GPU"))}
+        if w["kind"] == "1d":
+            cfg.update(n=w["n"], batch=w["batch"])
+        else:
+            cfg.update(shape=list(w["shape"]))
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
+            "dtype": "f64" if w["dtype"] == "c128" else "f32", "data": "synthetic", "config": cfg,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
+            "clocks": clk.result(),
+        }
+        print(json.dumps(line), flush=True)
+    if partitioned:
+        plan.close()
+        m.moa_fft_dist_finalize()
+    if dist:
+        td.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

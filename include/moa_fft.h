@@ -120,6 +120,17 @@ int64_t moa_fft_local_elems(moa_fft_plan_t plan);
 int moa_fft_launches_per_exec(moa_fft_plan_t plan);
 
 /*
+ * Per-pass timing with CUDA events on the exec stream (no host sync inside
+ * exec).  moa_fft_prof_begin arms the plan for up to max_execs execs: each
+ * exec records an event before every step (pass or all-to-all) and one after
+ * the last.  moa_fft_prof_end synchronises on the recorded events, writes the
+ * summed milliseconds of step i over all recorded execs to step_ms[i]
+ * (i < nsteps <= max_steps) and the number of execs to *execs, and disarms.
+ */
+moa_status_t moa_fft_prof_begin(moa_fft_plan_t plan, int max_execs);
+moa_status_t moa_fft_prof_end(moa_fft_plan_t plan, double *step_ms, int max_steps, int *nsteps, int *execs);
+
+/*
  * Processor-level lifting (ngpu > 1; SPMD, one process per GPU).
  *   moa_fft_get_unique_id : rank 0 creates the 128-byte NCCL unique id; the
  *                           caller broadcasts it (e.g. torch.distributed).

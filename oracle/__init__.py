@@ -110,6 +110,12 @@ def fft_radix2_rows(x, n: int) -> np.ndarray:
     return a
 
 
+def fft_radix2_rows_inplace(a: np.ndarray, n: int) -> np.ndarray:
+    assert a.dtype == np.complex128 and a.flags["C_CONTIGUOUS"] and a.size % n == 0
+    _check(_load().orc_fft_radix2_batch(a.ctypes.data, n, a.size // n), "fft_radix2_batch")
+    return a
+
+
 def dft_direct(x) -> np.ndarray:
     """O3: the O(n^2) definition with exact integer exponent reduction."""
     a = _c128(x)

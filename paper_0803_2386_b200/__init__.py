@@ -26,7 +26,7 @@ EXPORTS = [
     "moa_fft_destroy", "moa_fft_last_error", "moa_fft_local_elems", "moa_fft_launches_per_exec",
     "moa_fft_get_unique_id", "moa_fft_dist_init", "moa_fft_dist_finalize", "moa_fft_dist_loopback",
     "moa_fft_exec_loopback", "moa_dist_describe", "moa_psi_describe", "moa_psi_describe_3d",
-    "moa_plan_radices", "moa_fft_plan_describe",
+    "moa_plan_radices", "moa_fft_plan_describe", "moa_fft_prof_begin", "moa_fft_prof_end",
 ]
 
 
@@ -87,6 +87,8 @@ def _load():
         "moa_psi_describe_3d": [i64, i64, i64, i32, P(PassDesc), i32, P(i32)],
         "moa_plan_radices": [i64, i64, i32, P(i64), i32, P(i32)],
         "moa_fft_plan_describe": [vp, P(PassDesc), i32, P(i32)],
+        "moa_fft_prof_begin": [vp, i32],
+        "moa_fft_prof_end": [vp, P(ctypes.c_double), i32, P(i32), P(i32)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -217,6 +219,18 @@ def moa_fft_plan_describe(plan: int) -> list:
     np_ = ctypes.c_int()
     _check(lib.moa_fft_plan_describe(plan, out, MAX_PASSES, ctypes.byref(np_)))
     return [out[i].to_dict() for i in range(np_.value)]
+
+
+def moa_fft_prof_begin(plan: int, max_execs: int) -> None:
+    _check(lib.moa_fft_prof_begin(plan, max_execs))
+
+
+def moa_fft_prof_end(plan: int):
+    """-> (summed ms per step over the recorded execs, number of execs)."""
+    arr = (ctypes.c_double * 64)()
+    ns, nx = ctypes.c_int(), ctypes.c_int()
+    _check(lib.moa_fft_prof_end(plan, arr, 64, ctypes.byref(ns), ctypes.byref(nx)))
+    return list(arr[: ns.value]), nx.value
 
 
 def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128") -> dict:

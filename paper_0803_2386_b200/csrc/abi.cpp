@@ -46,7 +46,11 @@ struct moa_fft_plan_s {
     void *scratch = nullptr;
     void *staging = nullptr;
     DistPlan *dist = nullptr;  // processor-level lifting (comm.cpp)
+    // per-step event profiling (moa_fft_prof_begin / _end)
+    std::vector<cudaEvent_t> prof_ev;
+    int prof_max = 0, prof_count = 0, prof_nsteps = 0;
 };
+
 
 namespace {
 
@@ -72,13 +76,13 @@ void omega_ld(int64_t e, int64_t N, long double &re, long double &im) {
     im = -sinl(a);
 }
 
-moa_status_t upload_table(moa_fft_plan_s *p, const std::vector<long double> &v, const void **dptr) {
+moa_status_t upload_table(moa_fft_plan_s *p, const std::vector<long double> &v, const void **dptr, bool dbl = false) {
     const size_t cnt = v.size();
     void *d = nullptr;
-    moa_status_t st = dev_alloc(p, cnt * (p->dtype == MOA_C128 ? sizeof(double) : sizeof(float)), &d);
+    moa_status_t st = dev_alloc(p, cnt * ((dbl || p->dtype == MOA_C128) ? sizeof(double) : sizeof(float)), &d);
     if (st) return st;
     cudaError_t e;
-    if (p->dtype == MOA_C128) {
+    if (dbl || p->dtype == MOA_C128) {
         std::vector<double> h(cnt);
         for (size_t i = 0; i < cnt; i++) h[i] = (double)v[i];
         e = cudaMemcpy(d, h.data(), cnt * sizeof(double), cudaMemcpyHostToDevice);
@@ -124,9 +128,9 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
                 std::vector<long double> lo(2 * nlo), hi(2 * nhi);
                 for (int64_t e = 0; e < nlo; e++) omega_ld(e, d.twN, lo[2 * e], lo[2 * e + 1]);
                 for (int64_t e = 0; e < nhi; e++) omega_ld(e << h, d.twN, hi[2 * e], hi[2 * e + 1]);
-                moa_status_t st = upload_table(p, hi, &t.tw_hi);
+                moa_status_t st = upload_table(p, hi, &t.tw_hi, true);
                 if (st) return st;
-                st = upload_table(p, lo, &t.tw_lo);
+                st = upload_table(p, lo, &t.tw_lo, true);
                 if (st) return st;
                 byN[d.twN] = {t.tw_hi, t.tw_lo};
             }
@@ -293,15 +297,24 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (dev != p->device) return fail(MOA_EINVAL, "exec: the current device is not the plan's device");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (p->dist) return dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s);
-    for (size_t i = 0; i < p->passes.size(); i++) {
-        const moa_pass_desc_t &d = p->passes[i];
-        const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
-        void *dst = d.dst == 1 ? out : p->scratch;
-        e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
-        if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+    cudaEvent_t *evs = nullptr;
+    if (p->prof_count < p->prof_max) evs = &p->prof_ev[size_t(p->prof_count) * (p->prof_nsteps + 1)];
+    moa_status_t st = MOA_OK;
+    if (p->dist) {
+        st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs);
+    } else {
+        for (size_t i = 0; i < p->passes.size(); i++) {
+            const moa_pass_desc_t &d = p->passes[i];
+            const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
+            void *dst = d.dst == 1 ? out : p->scratch;
+            if (evs) cudaEventRecord(evs[i], s);
+            e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
+            if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+        }
+        if (evs) cudaEventRecord(evs[p->passes.size()], s);
     }
-    return MOA_OK;
+    if (evs) p->prof_count++;
+    return st;
 }
 
 moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host_out, void *stream) {
@@ -324,8 +337,58 @@ moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host
     return MOA_OK;
 }
 
+static int plan_nsteps(moa_fft_plan_t p) { return p->dist ? int(p->dist->steps.size()) : int(p->passes.size()); }
+
+static void prof_free(moa_fft_plan_t p) {
+    for (auto ev : p->prof_ev) cudaEventDestroy(ev);
+    p->prof_ev.clear();
+    p->prof_max = p->prof_count = 0;
+}
+
+moa_status_t moa_fft_prof_begin(moa_fft_plan_t p, int max_execs) {
+    if (!p || max_execs < 1 || max_execs > 100000) return fail(MOA_EINVAL, "prof_begin: bad arguments");
+    prof_free(p);
+    p->prof_nsteps = plan_nsteps(p);
+    const size_t cnt = size_t(max_execs) * (p->prof_nsteps + 1);
+    p->prof_ev.resize(cnt);
+    for (size_t i = 0; i < cnt; i++) {
+        cudaError_t e = cudaEventCreate(&p->prof_ev[i]);
+        if (e != cudaSuccess) {
+            p->prof_ev.resize(i);
+            prof_free(p);
+            return cuda_fail(e, "prof_begin: cudaEventCreate");
+        }
+    }
+    p->prof_max = max_execs;
+    p->prof_count = 0;
+    return MOA_OK;
+}
+
+moa_status_t moa_fft_prof_end(moa_fft_plan_t p, double *step_ms, int max_steps, int *nsteps, int *execs) {
+    if (!p || !step_ms || !nsteps || !execs) return fail(MOA_EINVAL, "prof_end: null argument");
+    const int ns = p->prof_nsteps;
+    if (ns > max_steps) return fail(MOA_EINVAL, "prof_end: step_ms too small");
+    for (int i = 0; i < ns; i++) step_ms[i] = 0.0;
+    for (int x = 0; x < p->prof_count; x++) {
+        cudaEvent_t *ev = &p->prof_ev[size_t(x) * (ns + 1)];
+        cudaError_t e = cudaEventSynchronize(ev[ns]);
+        if (e != cudaSuccess) return cuda_fail(e, "prof_end: sync");
+        for (int i = 0; i < ns; i++) {
+            float ms = 0.f;
+            e = cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            if (e != cudaSuccess) return cuda_fail(e, "prof_end: elapsed");
+            step_ms[i] += ms;
+        }
+    }
+    *nsteps = ns;
+    *execs = p->prof_count;
+    prof_free(p);
+    return MOA_OK;
+}
+
 moa_status_t moa_fft_destroy(moa_fft_plan_t p) {
     if (!p) return MOA_OK;
+    prof_free(p);
     for (void *a : p->allocs) cudaFree(a);
     if (p->dist) dist_plan_free(p->dist);
     delete p;

@@ -245,11 +245,14 @@ int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes) {
 }
 
 moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
-                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s) {
+                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
+                       cudaEvent_t *evs) {
     if (dp->loopback) return fail(MOA_EINVAL, "dist: a loopback plan runs through moa_fft_exec_loopback");
     if (!g_comm) return fail(MOA_EINVAL, "dist: no communicator (moa_fft_dist_init)");
     void *bufs[4] = {const_cast<void *>(in), out, scratch, dp->scratch2};
-    for (auto &st : dp->steps) {
+    for (size_t i = 0; i < dp->steps.size(); i++) {
+        const DistStep &st = dp->steps[i];
+        if (evs) cudaEventRecord(evs[i], s);
         if (st.kind == 0) {
             const moa_pass_desc_t &d = passes[st.pass];
             cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[d.dst], tabs[st.pass], s);
@@ -261,6 +264,7 @@ moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes,
             if (r != ncclSuccess) return nccl_fail(r, "all-to-all");
         }
     }
+    if (evs) cudaEventRecord(evs[dp->steps.size()], s);
     return MOA_OK;
 }
 

@@ -38,7 +38,8 @@ bool dist_ready(int ngpu);
 moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype);
 moa_status_t dist_plan_3d(DistPlan *&dp, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype);
 moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
-                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s);
+                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
+                       cudaEvent_t *evs);
 void dist_plan_free(DistPlan *dp);
 int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes);
 

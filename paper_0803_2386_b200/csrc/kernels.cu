@@ -192,21 +192,37 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
     }
 }
 
+// The steps of the line DFT.  Step 0 runs in the load mapping (line lA, index
+// tA), every later step in the store mapping (lB, tB): between steps the data
+// passes through shared memory anyway, so the thread <-> line assignment changes
+// for free there and no extra transposition is needed for a strided side.
 template <int LR, int LP, int LB, int S, int NSTEP, typename V>
-__device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm_line, int t, const V *__restrict__ twR) {
+__device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int lA, int tA, int lB, int tB,
+                                         const V *__restrict__ twR) {
     constexpr int LQ0 = LR - LP * (NSTEP - 1);  // the small radix goes first (no twiddles at NS = 1)
     constexpr int R = 1 << LR, P = 1 << LP;
     constexpr int LQ = S == 0 ? LQ0 : LP;
     constexpr int LNS = S == 0 ? 0 : LQ0 + LP * (S - 1);
     constexpr bool LAST = S == NSTEP - 1;
-    stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm_line, t, twR);
+    if constexpr (S == 0) stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lA * LS, tA, twR);
+    else stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lB * LS, tB, twR);
     if constexpr (!LAST) {
         __syncthreads();
+        const V *sl = sm + lB * LS;
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = sm_line[swz<LB>(t + m * (R / P))];
+        for (int m = 0; m < P; m++) pts[m] = sl[swz<LB>(tB + m * (R / P))];
         __syncthreads();
-        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm_line, t, twR);
+        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm, LS, lA, tA, lB, tB, twR);
     }
+}
+
+__device__ __forceinline__ double2 cvt_tw(double2 w, double2) { return w; }
+__device__ __forceinline__ float2 cvt_tw(double2 w, float2) { return make_float2(float(w.x), float(w.y)); }
+
+// w_N^e from the two-level double-precision table (exact integer exponent)
+__device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, const double2 *__restrict__ lo, int64_t e,
+                                             int h) {
+    return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((int64_t(1) << h) - 1))));
 }
 
 template <typename V, int LR>
@@ -223,74 +239,61 @@ __global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
 
     const int tid = threadIdx.x;
     const int64_t line0 = int64_t(blockIdx.x) * a.W;
-    // point-fast mapping: (l, t) with lanes over t inside one line
-    const int l = tid / TPL, t = tid % TPL;
-    V *sm_line = sm + l * a.LS;
+    // Thread mappings.  Point-fast: lanes over the points of one line (a side
+    // whose points are contiguous).  Line-fast: lanes over the W adjacent lines
+    // (a strided side: each warp request covers whole 128-byte runs).  A uses
+    // the load side's mapping, B the store side's.
+    const int lA = a.lf_load ? tid % a.W : tid / TPL, tA = a.lf_load ? tid / a.W : tid % TPL;
+    const int lB = a.lf_store ? tid % a.W : tid / TPL, tB = a.lf_store ? tid / a.W : tid % TPL;
+    int64_t io, oo, te, unused0, unused1;
+    line_offsets(a, line0 + lA, io, unused0, unused1);
+    line_offsets(a, line0 + lB, unused0, oo, te);
     V pts[P];
 
-    // ---- 1. load
-    if (a.lf_load) {
-        // line-fast mapping: lanes over the W adjacent lines (coalesced runs)
-        const int l2 = tid % a.W, t2 = tid / a.W;
-        int64_t io, oo, te;
-        line_offsets(a, line0 + l2, io, oo, te);
-        V tmp[P];
+    // ---- 1. load (128-bit, streaming)
 #pragma unroll
-        for (int m = 0; m < P; m++) tmp[m] = ld_stream(in + io + int64_t(t2 + m * TPL) * a.in_kstr);
-        V *sl2 = sm + l2 * a.LS;
+    for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(tA + m * TPL) * a.in_kstr);
+
+    // ---- 2. block butterflies (R-point DFT of every line); the mapping switches
+    //         from A to B at the first shared-memory exchange
+    bool moved = false;
+    if constexpr (LR > 0 && NSTEP > 1) {
+        if (!a.nodft) {
+            line_fft<LR, LP, LB, 0, NSTEP>(pts, sm, a.LS, lA, tA, lB, tB, twR);
+            moved = true;
+        }
+    } else if constexpr (LR > 0) {
+        if (!a.nodft) dft_reg<LR>(pts);
+    }
+    if (!moved && a.lf_load != a.lf_store) {  // single step: explicit transposition A -> B
+        V *sl = sm + lA * a.LS;
 #pragma unroll
-        for (int m = 0; m < P; m++) sl2[swz<LB>(t2 + m * TPL)] = tmp[m];
+        for (int m = 0; m < P; m++) sl[swz<LB>(tA + m * TPL)] = pts[m];
         __syncthreads();
+        const V *sl2 = sm + lB * a.LS;
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = sm_line[swz<LB>(t + m * TPL)];
-        __syncthreads();
-    } else {
-        int64_t io, oo, te;
-        line_offsets(a, line0 + l, io, oo, te);
-#pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(t + m * TPL) * a.in_kstr);
+        for (int m = 0; m < P; m++) pts[m] = sl2[swz<LB>(tB + m * TPL)];
     }
 
-    // ---- 2. block butterflies (R-point DFT of every line)
-    if constexpr (LR > 0) {
-        if (!a.nodft) line_fft<LR, LP, LB, 0, NSTEP>(pts, sm_line, t, twR);
-    }
-
-    // ---- 3. lifted weights w_N^{(e k) mod N}
+    // ---- 3. lifted weights w_N^{(e k) mod N} for k = tB + m R/P: one two-level
+    //         lookup for k = tB, one for the increment, then a multiplicative chain
+    //         in double precision (<= 15 products, ~1e-15 relative)
     if (a.twmask) {
-        int64_t io, oo, te;
-        line_offsets(a, line0 + l, io, oo, te);
-        const V *__restrict__ hi = reinterpret_cast<const V *>(a.tw_hi);
-        const V *__restrict__ lo = reinterpret_cast<const V *>(a.tw_lo);
-        const int64_t lomask = (int64_t(1) << a.twh) - 1;
+        const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
+        const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
+        const int64_t e0 = te + a.tw_off;
+        double2 w = tw_lookup(hi, lo, (e0 * tB) & a.twmask, a.twh);
+        const double2 ws = tw_lookup(hi, lo, (e0 * TPL) & a.twmask, a.twh);
 #pragma unroll
         for (int m = 0; m < P; m++) {
-            const int64_t k = t + m * TPL;
-            const int64_t e = ((te + a.tw_off) * k) & a.twmask;
-            if (e) {
-                const V w = cmul(__ldg(hi + (e >> a.twh)), __ldg(lo + (e & lomask)));
-                pts[m] = cmul(pts[m], w);
-            }
+            pts[m] = cmul(pts[m], cvt_tw(w, V{}));
+            if (m + 1 < P) w = cmul(w, ws);
         }
     }
 
-    // ---- 4. store
-    if (a.lf_store) {
+    // ---- 4. store (128-bit, streaming)
 #pragma unroll
-        for (int m = 0; m < P; m++) sm_line[swz<LB>(t + m * TPL)] = pts[m];
-        __syncthreads();
-        const int l2 = tid % a.W, t2 = tid / a.W;
-        int64_t io, oo, te;
-        line_offsets(a, line0 + l2, io, oo, te);
-        const V *sl2 = sm + l2 * a.LS;
-#pragma unroll
-        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, t2 + m * TPL), sl2[swz<LB>(t2 + m * TPL)]);
-    } else {
-        int64_t io, oo, te;
-        line_offsets(a, line0 + l, io, oo, te);
-#pragma unroll
-        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, t + m * TPL), pts[m]);
-    }
+    for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, tB + m * TPL), pts[m]);
 }
 
 template <typename V> using KFn = void (*)(const KArgs);
