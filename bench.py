@@ -286,31 +286,43 @@ def main():
     # ---- roofline of the dominant kernel
     peak, peak_src = load_peaks()
     desc = plan.describe()
-    kinds = []
+    vt = "double2" if w["dtype"] == "c128" else "float2"
+    launches_l = []                              # one entry per timed step of an exec
     if partitioned:
         sched = m.moa_dist_describe(rank, world, w["shape"] if w["kind"] == "3d" else w["n"], w["dtype"])
-        kinds = [s[0] for s in sched["steps"]]
+        for s in sched["steps"]:
+            if s[0] == "pass":
+                launches_l.append(("pass", f"pass_kernel<{vt},{sched['passes'][s[1]]['logR']}>"))
+            else:
+                launches_l.append(("alltoall", "ncclAlltoAll"))
     else:
-        kinds = ["pass"] * len(desc)
+        i = 0
+        while i < len(desc):
+            if desc[i]["ring"] == 2:
+                launches_l.append(("pair", f"pair_kernel<{vt},{desc[i]['logR']},{desc[i + 1]['logR']}>"))
+                i += 2
+            else:
+                launches_l.append(("pass", f"pass_kernel<{vt},{desc[i]['logR']}>"))
+                i += 1
+    kinds = [k for k, _ in launches_l]
     per_step = [s / max(nexec, 1) for s in step_ms_list]
-    pass_idx = [i for i, k in enumerate(kinds) if k == "pass"]
+    pass_idx = [i for i, k in enumerate(kinds) if k != "alltoall"]
     dom = max(pass_idx, key=lambda i: per_step[i])
     dom_ms = per_step[dom]
-    dom_bytes = 2 * data_bytes                   # one HBM round trip of the local array per pass launch
+    dom_bytes = 2 * data_bytes                   # one HBM round trip of the local array per launch
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     alg_bytes = ALG_PASSES[args.workload] * 2 * data_bytes
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
-        traffic = tr.get(args.workload, {}).get(str(dom))
+        traffic = tr.get(args.workload, {}).get(launches_l[dom][1])
     except Exception:
         pass
-    pdesc = desc[pass_idx.index(dom)] if not partitioned else sched["passes"][[s[1] for s in sched["steps"] if s[0] == "pass"][pass_idx.index(dom)]]
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4), "traffic": traffic,
-        "kernel": f"pass_kernel<{'double2' if w['dtype'] == 'c128' else 'float2'},{pdesc['logR']}> (step {dom})",
+        "kernel": f"{launches_l[dom][1]} (step {dom})",
         "kernel_ms": round(dom_ms, 4), "kernel_alg_bytes": dom_bytes, "peak_source": peak_src,
         "step_alg_bytes": alg_bytes,
         "step_frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peak, 4),

@@ -197,6 +197,14 @@ typedef struct {
     int32_t smem_bytes;         /* dynamic shared memory per CTA */
     int32_t line_pad;           /* smem line stride = R + line_pad elements */
     int32_t src, dst;           /* buffer ids: 0 = in, 1 = out, 2 = scratch, 3 = scratch2 */
+    /* L2-staged pass pair (the lifting at the L2 level): ring = 2 marks pass A,
+     * whose output goes to a ring of ring_slots group buffers of ring_G
+     * elements; ring = 1 marks the following pass B, which reads it back.  The
+     * last line digit is the group; its stride on the ring side is replaced by
+     * (group mod ring_slots) * ring_G.  ring_lag: groups between A and B in the
+     * tile order.  ring_discard: B drops the consumed lines from L2 (no write-back). */
+    int32_t ring, ring_slots, ring_lag, ring_discard;
+    int64_t ring_groups, ring_G;
 } moa_pass_desc_t;
 
 /* ONF descriptors of a 1-D lifting (radices == NULL: the planner's choice). */

@@ -43,6 +43,8 @@ class PassDesc(ctypes.Structure):
         ("lf_load", ctypes.c_int32), ("lf_store", ctypes.c_int32),
         ("W", ctypes.c_int32), ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
         ("line_pad", ctypes.c_int32), ("src", ctypes.c_int32), ("dst", ctypes.c_int32),
+        ("ring", ctypes.c_int32), ("ring_slots", ctypes.c_int32), ("ring_lag", ctypes.c_int32),
+        ("ring_discard", ctypes.c_int32), ("ring_groups", ctypes.c_int64), ("ring_G", ctypes.c_int64),
     ]
 
     def to_dict(self) -> dict:
@@ -53,7 +55,9 @@ class PassDesc(ctypes.Structure):
                     twN=self.twN, tw_off=self.tw_off, out_ksplit=self.out_ksplit,
                     out_kstr_hi=self.out_kstr_hi, nodft=self.nodft, lf_load=self.lf_load,
                     lf_store=self.lf_store, W=self.W, threads=self.threads,
-                    smem_bytes=self.smem_bytes, line_pad=self.line_pad, src=self.src, dst=self.dst)
+                    smem_bytes=self.smem_bytes, line_pad=self.line_pad, src=self.src, dst=self.dst,
+                    ring=self.ring, ring_slots=self.ring_slots, ring_lag=self.ring_lag,
+                    ring_discard=self.ring_discard, ring_groups=self.ring_groups, ring_G=self.ring_G)
 
 
 class MoaError(RuntimeError):

@@ -46,6 +46,7 @@ struct moa_fft_plan_s {
     void *scratch = nullptr;
     void *staging = nullptr;
     DistPlan *dist = nullptr;  // processor-level lifting (comm.cpp)
+    std::vector<RingState> rings;  // rings[i] valid where passes[i].ring == 2
     // per-step event profiling (moa_fft_prof_begin / _end)
     std::vector<cudaEvent_t> prof_ev;
     int prof_max = 0, prof_count = 0, prof_nsteps = 0;
@@ -176,6 +177,22 @@ moa_status_t finish_plan(moa_fft_plan_s *p) {
         moa_status_t st = dev_alloc(p, size_t(p->local_elems) * p->esize, &p->scratch);
         if (st) return st;
     }
+    p->rings.assign(p->passes.size(), RingState{});
+    for (size_t i = 0; i < p->passes.size(); i++) {
+        const moa_pass_desc_t &d = p->passes[i];
+        if (d.ring != 2) continue;
+        if (i + 1 >= p->passes.size() || p->passes[i + 1].ring != 1) return fail(MOA_EINVAL, "plan: unpaired ring pass");
+        RingState &r = p->rings[i];
+        void *ctr = nullptr;
+        moa_status_t st = dev_alloc(p, size_t(d.ring_slots) * d.ring_G * p->esize, &r.ring);
+        if (!st) st = dev_alloc(p, sizeof(unsigned long long) * (2 * size_t(d.ring_groups) + 1), &ctr);
+        if (st) return st;
+        e = cudaMemset(ctr, 0, sizeof(unsigned long long) * (2 * size_t(d.ring_groups) + 1));
+        if (e != cudaSuccess) return cuda_fail(e, "ring counters");
+        r.qctr = static_cast<unsigned long long *>(ctr);
+        r.cntA = r.qctr + 1;
+        r.cntB = r.cntA + d.ring_groups;
+    }
     return build_tables(p);
 }
 
@@ -217,7 +234,7 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
             st = parse_lift_env(n, rad, have);
             if (!st && !have) st = plan_radices(n, batch, dtype, rad);
         }
-        if (!st) st = psi_lift_passes(n, batch, dtype, rad.data(), int(rad.size()), p->passes);
+        if (!st) st = psi_build(n, batch, dtype, rad, radices == nullptr, p->passes);
     }
     if (!st) st = finish_plan(p);
     if (st) {
@@ -303,15 +320,26 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     if (p->dist) {
         st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs);
     } else {
-        for (size_t i = 0; i < p->passes.size(); i++) {
+        int step = 0;
+        for (size_t i = 0; i < p->passes.size(); i++, step++) {
             const moa_pass_desc_t &d = p->passes[i];
             const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
-            void *dst = d.dst == 1 ? out : p->scratch;
-            if (evs) cudaEventRecord(evs[i], s);
-            e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
-            if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+            if (evs) cudaEventRecord(evs[step], s);
+            if (d.ring == 2) {  // fused pair: passes i and i+1 in one launch, intermediate in the L2 ring
+                const moa_pass_desc_t &dB = p->passes[i + 1];
+                void *dst = dB.dst == 1 ? out : p->scratch;
+                RingState &r = p->rings[i];
+                e = launch_pair(d, dB, p->dtype, src, dst, r, p->tabs[i], p->tabs[i + 1], s);
+                if (e != cudaSuccess) return cuda_fail(e, "pass-pair kernel launch");
+                r.epoch++;
+                i++;
+            } else {
+                void *dst = d.dst == 1 ? out : p->scratch;
+                e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
+                if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+            }
         }
-        if (evs) cudaEventRecord(evs[p->passes.size()], s);
+        if (evs) cudaEventRecord(evs[step], s);
     }
     if (evs) p->prof_count++;
     return st;
@@ -337,7 +365,13 @@ moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host
     return MOA_OK;
 }
 
-static int plan_nsteps(moa_fft_plan_t p) { return p->dist ? int(p->dist->steps.size()) : int(p->passes.size()); }
+static int local_launches(moa_fft_plan_t p) {
+    int c = 0;
+    for (auto &d : p->passes) c += d.ring != 1;  // a fused pair is one launch
+    return c;
+}
+
+static int plan_nsteps(moa_fft_plan_t p) { return p->dist ? int(p->dist->steps.size()) : local_launches(p); }
 
 static void prof_free(moa_fft_plan_t p) {
     for (auto ev : p->prof_ev) cudaEventDestroy(ev);
@@ -399,7 +433,7 @@ int64_t moa_fft_local_elems(moa_fft_plan_t p) { return p ? p->local_elems : -1; 
 
 int moa_fft_launches_per_exec(moa_fft_plan_t p) {
     if (!p) return -1;
-    return p->dist ? dist_launches(p->dist, p->passes) : int(p->passes.size());
+    return p->dist ? dist_launches(p->dist, p->passes) : local_launches(p);
 }
 
 moa_status_t moa_psi_describe(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
@@ -413,7 +447,7 @@ moa_status_t moa_psi_describe(int64_t n, int64_t batch, moa_dtype_t dtype, const
     else st = plan_radices(n, batch, dtype, rad);
     if (st) return st;
     std::vector<moa_pass_desc_t> v;
-    st = psi_lift_passes(n, batch, dtype, rad.data(), int(rad.size()), v);
+    st = psi_build(n, batch, dtype, rad, radices == nullptr, v);
     if (st) return st;
     if (int(v.size()) > max_passes) return fail(MOA_EINVAL, "describe: output array too small");
     for (size_t i = 0; i < v.size(); i++) out[i] = v[i];

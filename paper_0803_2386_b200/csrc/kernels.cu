@@ -133,6 +133,8 @@ struct KArgs {
     int32_t nodft;
     int32_t W, LS;   // lines per tile, smem line stride (elements)
     int32_t lf_load, lf_store;
+    int32_t ring;     // 0: HBM both sides; 1: loads from the L2 ring; 2: stores to the ring
+    int32_t discard;  // ring == 1: discard the consumed ring lines (no write-back)
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -225,20 +227,20 @@ __device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, con
     return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((int64_t(1) << h) - 1))));
 }
 
+// One tile (W adjacent lines starting at line0) of a pass.  ring >= 0: the
+// ring slot of this tile's group (the L2-staged intermediate of a fused pass
+// pair, see pair_kernel); the ring side's address gets slot * ringG added.
 template <typename V, int LR>
-__global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
+__device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
     constexpr int LP = LR < 4 ? LR : 4;
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
     constexpr int NSTEP = LR == 0 ? 1 : (LR + LP - 1) / LP;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    V *sm = reinterpret_cast<V *>(smem_raw);
     const V *__restrict__ in = reinterpret_cast<const V *>(a.in);
     V *__restrict__ out = reinterpret_cast<V *>(a.out);
     const V *__restrict__ twR = reinterpret_cast<const V *>(a.twR);
 
     const int tid = threadIdx.x;
-    const int64_t line0 = int64_t(blockIdx.x) * a.W;
     // Thread mappings.  Point-fast: lanes over the points of one line (a side
     // whose points are contiguous).  Line-fast: lanes over the W adjacent lines
     // (a strided side: each warp request covers whole 128-byte runs).  A uses
@@ -248,11 +250,18 @@ __global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
     int64_t io, oo, te, unused0, unused1;
     line_offsets(a, line0 + lA, io, unused0, unused1);
     line_offsets(a, line0 + lB, unused0, oo, te);
+    if (a.ring == 1) io += ring_off;
+    if (a.ring == 2) oo += ring_off;
     V pts[P];
 
-    // ---- 1. load (128-bit, streaming)
+    // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
+    if (a.ring == 1) {
 #pragma unroll
-    for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(tA + m * TPL) * a.in_kstr);
+        for (int m = 0; m < P; m++) pts[m] = __ldcg(in + io + int64_t(tA + m * TPL) * a.in_kstr);
+    } else {
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(tA + m * TPL) * a.in_kstr);
+    }
 
     // ---- 2. block butterflies (R-point DFT of every line); the mapping switches
     //         from A to B at the first shared-memory exchange
@@ -275,6 +284,20 @@ __global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
         for (int m = 0; m < P; m++) pts[m] = sl2[swz<LB>(tB + m * TPL)];
     }
 
+    // ---- ring: every thread has consumed its loads (the exchanges above, or the
+    //      barrier here); drop the ring lines this tile read from L2 without a
+    //      write-back (discard.global.L2): the intermediate never reaches HBM
+    if (a.ring == 1 && a.discard) {
+        __syncthreads();
+        constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+            const V *p = in + io + int64_t(tA + m * TPL) * a.in_kstr;
+            if ((reinterpret_cast<uintptr_t>(p) & 127) == 0 && (a.in_kstr != 1 || ((tA + m * TPL) % EPL) == 0))
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+        }
+    }
+
     // ---- 3. lifted weights w_N^{(e k) mod N} for k = tB + m R/P: one two-level
     //         lookup for k = tB, one for the increment, then a multiplicative chain
     //         in double precision (<= 15 products, ~1e-15 relative)
@@ -291,34 +314,124 @@ __global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
         }
     }
 
-    // ---- 4. store (128-bit, streaming)
+    // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
+    if (a.ring == 2) {
 #pragma unroll
-    for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, tB + m * TPL), pts[m]);
+        for (int m = 0; m < P; m++) out[oo + kaddr(a, tB + m * TPL)] = pts[m];
+    } else {
+#pragma unroll
+        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, tB + m * TPL), pts[m]);
+    }
+}
+
+template <typename V, int LR>
+__global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<V *>(smem_raw), 0);
+}
+
+// A fused pass pair: pass A writes its output to an L2-resident ring of
+// `slots` group buffers, pass B reads it from there -- the lifting applied at
+// the L2 level, so the intermediate never makes an HBM round trip (the
+// paper's "each block fits one level of the hierarchy").
+// Tiles are handed out in a fixed order by an atomic queue (A tiles of group g,
+// interleaved with B tiles of group g - lag); a B tile waits for its group's A
+// tiles, an A tile reusing a slot waits for the previous group's B tiles.
+// Every waited-on tile was dequeued earlier by a running CTA, so the waits
+// cannot deadlock (the decoupled look-back argument).
+struct PairArgs {
+    KArgs A, B;
+    int64_t groups, ringG;
+    int32_t TA, TB, lag, slot_mask;
+    unsigned long long *qctr, *cntA, *cntB;
+    unsigned long long epoch;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename V, int LRA, int LRB>
+__global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ long long s_pos;
+    const int64_t G = p.groups, L = p.lag, T = p.TA + p.TB;
+    if (threadIdx.x == 0) s_pos = (long long)(atomicAdd(p.qctr, 1ull) - p.epoch * (unsigned long long)(G * T));
+    __syncthreads();
+    int64_t pos = s_pos;
+    bool isB;
+    int64_t g, idx;
+    const int64_t n1 = (L < G ? L : G) * p.TA;
+    if (pos < n1) {
+        isB = false;
+        g = pos / p.TA;
+        idx = pos % p.TA;
+    } else {
+        pos -= n1;
+        const int64_t n2 = G > L ? (G - L) * T : 0;
+        if (pos < n2) {
+            const int64_t s = L + pos / T, r = pos % T;
+            isB = r >= p.TA;
+            g = isB ? s - L : s;
+            idx = isB ? r - p.TA : r;
+        } else {
+            pos -= n2;
+            isB = true;
+            g = (G > L ? G - L : 0) + pos / p.TB;
+            idx = pos % p.TB;
+        }
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long round = p.epoch + 1;
+        if (isB) {
+            while (ld_acquire(p.cntA + g) < round * (unsigned long long)p.TA) __nanosleep(100);
+        } else if (g > p.slot_mask) {
+            while (ld_acquire(p.cntB + g - (p.slot_mask + 1)) < round * (unsigned long long)p.TB) __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    const int64_t ring_off = (g & p.slot_mask) * p.ringG;
+    V *sm = reinterpret_cast<V *>(smem_raw);
+    if (isB) tile_body<V, LRB>(p.B, (g * p.TB + idx) * p.B.W, sm, ring_off);
+    else tile_body<V, LRA>(p.A, (g * p.TA + idx) * p.A.W, sm, ring_off);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(isB ? p.cntB + g : p.cntA + g, 1ull);
+    }
 }
 
 template <typename V> using KFn = void (*)(const KArgs);
+template <typename V> using PFn = void (*)(const PairArgs);
 
 template <typename V, int... Ls> constexpr auto make_table(std::integer_sequence<int, Ls...>) {
     return std::array<KFn<V>, sizeof...(Ls)>{&pass_kernel<V, Ls>...};
 }
+// fused pairs: R_A, R_B in 2^5 .. 2^10 (36 instantiations per dtype)
+template <typename V, int... Is> constexpr auto make_pair_table(std::integer_sequence<int, Is...>) {
+    return std::array<PFn<V>, sizeof...(Is)>{&pair_kernel<V, 5 + Is / 6, 5 + Is % 6>...};
+}
+const std::array<PFn<double2>, 36> kPair128 = make_pair_table<double2>(std::make_integer_sequence<int, 36>{});
+const std::array<PFn<float2>, 36> kPair64 = make_pair_table<float2>(std::make_integer_sequence<int, 36>{});
 const std::array<KFn<double2>, 13> kTab128 = make_table<double2>(std::make_integer_sequence<int, 13>{});
 const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
 
-template <typename V>
-cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
-                     const DevTables &tb, cudaStream_t stream) {
+KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines) {
     KArgs a{};
     a.in = in;
     a.out = out;
     a.ndig = d.ndig;
-    int64_t nlines = 1;
+    int64_t nl = 1;
     for (int i = 0; i < d.ndig; i++) {
         a.in_str[i] = d.in_str[i];
         a.out_str[i] = d.out_str[i];
         a.tw_str[i] = d.tw_str[i];
         a.lext[i] = log2_exact(d.ext[i]);
-        nlines *= d.ext[i];
+        nl *= d.ext[i];
     }
+    *nlines = nl;
     a.in_kstr = d.in_kstr;
     a.out_kstr = d.out_kstr;
     a.twR = tb.twR;
@@ -335,6 +448,16 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     a.LS = (1 << d.logR) + d.line_pad;
     a.lf_load = d.lf_load;
     a.lf_store = d.lf_store;
+    a.ring = d.ring;
+    a.discard = d.ring_discard;
+    return a;
+}
+
+template <typename V>
+cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
+                     const DevTables &tb, cudaStream_t stream) {
+    int64_t nlines = 0;
+    KArgs a = fill_args(d, in, out, tb, &nlines);
     KFn<V> fn = tab[d.logR];
     if (d.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
@@ -344,6 +467,35 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
     return cudaGetLastError();
 }
+
+template <typename V>
+cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc_t &dA, const moa_pass_desc_t &dB,
+                          const void *in, void *out, const RingState &rs, const DevTables &tA, const DevTables &tB,
+                          cudaStream_t stream) {
+    int64_t nA = 0, nB = 0;
+    PairArgs p{};
+    p.A = fill_args(dA, in, rs.ring, tA, &nA);
+    p.B = fill_args(dB, rs.ring, out, tB, &nB);
+    p.TA = int32_t((nA / dA.W) / dA.ring_groups);
+    p.TB = int32_t((nB / dB.W) / dB.ring_groups);
+    p.groups = dA.ring_groups;
+    p.ringG = dA.ring_G;
+    p.lag = dA.ring_lag;
+    p.slot_mask = dA.ring_slots - 1;
+    p.qctr = rs.qctr;
+    p.cntA = rs.cntA;
+    p.cntB = rs.cntB;
+    p.epoch = rs.epoch;
+    PFn<V> fn = tab[(dA.logR - 5) * 6 + (dB.logR - 5)];
+    const int smem = dA.smem_bytes > dB.smem_bytes ? dA.smem_bytes : dB.smem_bytes;
+    if (smem > 48 * 1024 - 64) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t tiles = p.groups * (p.TA + p.TB);
+    fn<<<dim3(unsigned(tiles)), dim3(unsigned(dA.threads)), size_t(smem), stream>>>(p);
+    return cudaGetLastError();
+}
 }  // namespace
 
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
@@ -351,6 +503,14 @@ cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void 
     if (d.logR < 0 || d.logR > 12) return cudaErrorInvalidValue;
     if (dtype == MOA_C128) return launch_t<double2>(kTab128, d, in, out, tab, stream);
     return launch_t<float2>(kTab64, d, in, out, tab, stream);
+}
+
+cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
+                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream) {
+    if (dA.logR < 5 || dA.logR > 10 || dB.logR < 5 || dB.logR > 10 || dA.threads != dB.threads)
+        return cudaErrorInvalidValue;
+    if (dtype == MOA_C128) return launch_pair_t<double2>(kPair128, dA, dB, in, out, rs, tA, tB, stream);
+    return launch_pair_t<float2>(kPair64, dA, dB, in, out, rs, tA, tB, stream);
 }
 
 cudaError_t kernel_attributes(moa_dtype_t dtype, int logR, int *max_threads, int *regs) {

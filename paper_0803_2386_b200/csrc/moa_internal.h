@@ -40,9 +40,28 @@ struct DevTables {
     const void *tw_hi = nullptr; // w_N^{eh 2^h}
     const void *tw_lo = nullptr; // w_N^{el}
 };
+// Device state of the L2 ring of a fused pass pair (owned by the plan).
+struct RingState {
+    void *ring = nullptr;                 // ring_slots * ring_G elements
+    unsigned long long *qctr = nullptr;   // tile queue (epoch-based, never reset)
+    unsigned long long *cntA = nullptr;   // per-group completed A tiles
+    unsigned long long *cntB = nullptr;   // per-group completed B tiles
+    unsigned long long epoch = 0;         // execs of this pair so far
+};
 int log2_exact(int64_t n);
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out,
                         const DevTables &tab, cudaStream_t stream);
+cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
+                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream);
+// psi.cpp: fuse the passes of a one-GPU lifting into L2-staged pairs where the
+// group working set fits (marks ring fields; returns how many pairs were made)
+int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,
+                   moa_dtype_t dtype);
+// The descriptors a 1-D plan runs: a planned 4-factor lifting (or any
+// 4-factor lifting with MOA_FFT_LIFT4=1) as two fused pairs, otherwise the
+// plain passes with the 2-pass fusion where it applies.
+moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::vector<int64_t> &radices, bool planned,
+                       std::vector<moa_pass_desc_t> &out);
 cudaError_t kernel_attributes(moa_dtype_t dtype, int logR, int *max_threads, int *regs);
 
 }  // namespace moa

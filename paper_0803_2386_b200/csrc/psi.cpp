@@ -20,6 +20,7 @@
 // transformed weights of the lifted level).  The last pass
 // transforms the contiguous rows and stores through the axis-reversing
 // transpose (the lifted final transpose), giving natural order.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -51,6 +52,8 @@ static void add_digit(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, i
     d.ndig++;
 }
 
+static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W);
+
 void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int esize = dtype == MOA_C128 ? 16 : 8;
     const int slots = 128 / esize;        // elements per 128-byte smem row / DRAM line
@@ -64,6 +67,24 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int64_t smem_cap = 100 * 1024;  // two CTAs per SM
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
+    set_tile(d, dtype, W);
+}
+
+// a legal tile of exactly W lines? (used to give both passes of a fused pair the same CTA size)
+static bool tile_ok(const moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
+    const int esize = dtype == MOA_C128 ? 16 : 8;
+    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int64_t R = int64_t(1) << logR, TPL = R >> logP;
+    const int64_t ext0 = d.ndig ? d.ext[0] : 1;
+    return W >= 1 && W * TPL <= 512 && W * R * esize <= 100 * 1024 && ext0 % W == 0;
+}
+
+static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
+    const int esize = dtype == MOA_C128 ? 16 : 8;
+    const int slots = 128 / esize;
+    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int64_t R = int64_t(1) << logR, TPL = R >> logP;
+    const bool lf = d.lf_load || d.lf_store;
     d.W = int32_t(W);
     d.threads = int32_t(W * TPL);
     int64_t pad;
@@ -200,6 +221,171 @@ moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, 
     return MOA_OK;
 }
 
+// L2-level lifting: a two-pass lifting of many independent
+// rows (the cfg2 shape) becomes one fused pass pair whose intermediate lives in
+// an L2-resident ring of row buffers.  Group = one row: pass A's lines (the
+// strided columns j of row b) and pass B's lines (the rows k_0 of row b) both
+// have the row b as their last (slowest) digit; on the ring side that digit's
+// stride becomes (b mod slots) * n.
+int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,
+                   moa_dtype_t dtype) {
+    const char *env = std::getenv("MOA_FFT_FUSE");
+    if (env && env[0] == '0') return 0;
+    const int64_t esize = dtype == MOA_C128 ? 16 : 8;
+    if (passes.size() != 2 || radices.size() != 2) return 0;
+    moa_pass_desc_t &A = passes[0], &B = passes[1];
+    const int64_t gbytes = n * esize;
+    if (batch < 16 || gbytes > (int64_t(8) << 20)) return 0;
+    if (A.logR < 5 || A.logR > 10 || B.logR < 5 || B.logR > 10) return 0;
+    if (A.ndig != 2 || B.ndig != 2) return 0;
+    if (A.threads != B.threads) {  // equalise the CTA size by widening the narrower tile
+        moa_pass_desc_t &lo = A.threads < B.threads ? A : B;
+        const moa_pass_desc_t &hi = A.threads < B.threads ? B : A;
+        const int64_t W = int64_t(lo.W) * hi.threads / lo.threads;
+        if (!tile_ok(lo, dtype, W)) return 0;
+        set_tile(lo, dtype, W);
+        if (A.threads != B.threads) return 0;
+    }
+    if (A.ext[1] != batch || B.ext[1] != batch) return 0;
+    int64_t slots = 4;
+    while (slots * 2 * gbytes <= (int64_t(32) << 20) && slots < 64) slots *= 2;
+    for (moa_pass_desc_t *d : {&A, &B}) {
+        d->ring_slots = int32_t(slots);
+        d->ring_lag = int32_t(slots / 2);
+        d->ring_discard = 1;
+        d->ring_groups = batch;
+        d->ring_G = n;
+    }
+    A.ring = 2;
+    A.out_str[1] = 0;  // the group digit addresses the ring slot
+    A.dst = -1;
+    B.ring = 1;
+    B.in_str[1] = 0;
+    B.src = -1;
+    if (env && env[0] == '2') A.ring_discard = B.ring_discard = 0;
+    return 1;
+}
+
+// Four-pass lifting n = R0 R1 R2 R3 run as two L2-staged pairs, so a single
+// huge transform costs two HBM round trips (SURVEY §8(d.3)'s count for the
+// 2^14 x 2^14 / 2^15 x 2^15 six-step) with every per-CTA block <= 2^10 points.
+//   pair (0,1): group = W consecutive j' (j = i1 S1 + j', S1 = R2 R3); pass 0
+//     lines (l, i1 | g, b), pass 1 lines (l, k0 | g, b); ring layout
+//     [(k0 R1 + i1) W + l]; pass 1 writes the global intermediate.
+//   pair (2,3): group = (k1, k0 >> log2 W); pass 2 lines (j, l, k1 | g0, b) with
+//     l = k0 mod W, pass 3 lines (l, k2, k1 | g0, b); ring layout
+//     [(l R2 + k2) R3 + i3]; pass 3 stores natural order
+//     X[k0 + R0 k1 + R0 R1 k2 + R0 R1 R2 k3].
+// Digits after `|` are the group (the slowest line bits); their ring-side
+// strides are 0 (the slot offset replaces them).
+static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *R,
+                                std::vector<moa_pass_desc_t> &out) {
+    out.clear();
+    const int64_t esize = dtype == MOA_C128 ? 16 : 8;
+    const int64_t W = 128 / esize;
+    const int64_t R0 = R[0], R1 = R[1], R2 = R[2], R3 = R[3];
+    const int64_t S1 = R2 * R3, S0 = R1 * S1, N1 = S0, N2 = S1;
+    if (R0 < W || S1 < W || R3 < W) return fail(MOA_EUNSUPPORTED, "psi: lift4 needs R0, R3 >= W");
+    const int64_t G01 = R0 * R1 * W, G23 = W * R2 * R3;
+    const int64_t g01 = (S1 / W) * batch, g23 = R1 * (R0 / W) * batch;
+    auto ring = [&](moa_pass_desc_t &d, int side, int64_t groups, int64_t G) {
+        int64_t slots = 4;
+        while (slots * 2 * G * esize <= (int64_t(32) << 20) && slots < 64 && slots * 2 <= groups) slots *= 2;
+        d.ring = side;
+        d.ring_slots = int32_t(slots);
+        d.ring_lag = int32_t(slots / 2);
+        d.ring_discard = 1;
+        d.ring_groups = groups;
+        d.ring_G = G;
+    };
+    moa_pass_desc_t d;
+    // pass 0: in -> ring
+    desc_init(d, log2_exact(R0));
+    add_digit(d, W, 1, 1, 1);                 // l   (j' = g W + l)
+    add_digit(d, R1, S1, W, S1);              // i1
+    add_digit(d, S1 / W, W, 0, W);            // g   (group)
+    add_digit(d, batch, n, 0, 0);             // b   (group)
+    d.in_kstr = S0;
+    d.out_kstr = R1 * W;
+    d.twN = n;
+    d.lf_load = d.lf_store = 1;
+    d.src = 0;
+    d.dst = -1;
+    ring(d, 2, g01, G01);
+    out.push_back(d);
+    // pass 1: ring -> scratch (global intermediate, position k0 N1 + k1 S1 + j')
+    desc_init(d, log2_exact(R1));
+    add_digit(d, W, 1, 1, 1);                 // l
+    add_digit(d, R0, R1 * W, N1, 0);          // k0
+    add_digit(d, S1 / W, 0, W, W);            // g
+    add_digit(d, batch, 0, n, 0);             // b
+    d.in_kstr = W;
+    d.out_kstr = S1;
+    d.twN = N1;
+    d.lf_load = d.lf_store = 1;
+    d.src = -1;
+    d.dst = 2;
+    ring(d, 1, g01, G01);
+    out.push_back(d);
+    // pass 2: scratch -> ring (lines o = k0 R1 + k1, j = i3)
+    desc_init(d, log2_exact(R2));
+    add_digit(d, R3, 1, 1, 1);                // j
+    add_digit(d, W, R1 * N2, R2 * R3, 0);     // l = k0 mod W
+    add_digit(d, R1, N2, 0, 0);               // k1        (group)
+    add_digit(d, R0 / W, W * R1 * N2, 0, 0);  // g0 = k0 / W (group)
+    add_digit(d, batch, n, 0, 0);             // b         (group)
+    d.in_kstr = R3;
+    d.out_kstr = R3;
+    d.twN = N2;
+    d.lf_load = d.lf_store = 1;
+    d.src = 2;
+    d.dst = -1;
+    ring(d, 2, g23, G23);
+    out.push_back(d);
+    // pass 3: ring -> out, natural order
+    desc_init(d, log2_exact(R3));
+    add_digit(d, W, R2 * R3, 1, 0);           // l
+    add_digit(d, R2, R3, R0 * R1, 0);         // k2
+    add_digit(d, R1, 0, R0, 0);               // k1
+    add_digit(d, R0 / W, 0, W, 0);            // g0
+    add_digit(d, batch, 0, n, 0);             // b
+    d.in_kstr = 1;
+    d.out_kstr = R0 * R1 * R2;
+    d.lf_load = 0;
+    d.lf_store = 1;
+    d.src = -1;
+    d.dst = 1;
+    ring(d, 1, g23, G23);
+    out.push_back(d);
+    for (auto &x : out) psi_choose_tile(x, dtype);
+    // both passes of a pair need one CTA size: widen the narrower tile
+    for (int p = 0; p < 4; p += 2) {
+        moa_pass_desc_t &A = out[p], &B = out[p + 1];
+        if (A.W != W || B.W != W) return fail(MOA_EUNSUPPORTED, "psi: lift4 tile must cover W lines");
+        if (A.threads != B.threads) return fail(MOA_EUNSUPPORTED, "psi: lift4 pair CTA sizes differ");
+    }
+    return MOA_OK;
+}
+
+moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::vector<int64_t> &radices, bool planned,
+                       std::vector<moa_pass_desc_t> &out) {
+    const char *fz = std::getenv("MOA_FFT_FUSE");
+    const char *l4 = std::getenv("MOA_FFT_LIFT4");
+    const bool fuse = !(fz && fz[0] == '0');
+    if (fuse && radices.size() == 4 && (planned || (l4 && l4[0] == '1')) && radices[0] == radices[1] &&
+        radices[2] == radices[3]) {
+        std::vector<moa_pass_desc_t> v;
+        if (lift4_fused(n, batch, dtype, radices.data(), v) == MOA_OK) {
+            out.swap(v);
+            return MOA_OK;
+        }
+    }
+    moa_status_t st = psi_lift_passes(n, batch, dtype, radices.data(), int(radices.size()), out);
+    if (st) return st;
+    psi_fuse_pairs(out, radices, n, batch, dtype);
+    return MOA_OK;
+}
+
 // Planner (step a1): the fewest passes whose per-pass line fits one CTA tile,
 // radices as equal as possible (largest first) so every pass is one HBM round
 // trip of similar cost.  Per-CTA limit: 2^9 points for the line-coalesced
@@ -213,6 +399,14 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
     const int max_mid = dtype == MOA_C128 ? 9 : 10;  // strided passes: W adjacent lines per tile
     if (t <= max_single) {
         radices.push_back(n);
+        return MOA_OK;
+    }
+    // large transforms: four factors (R, R, R', R') run as two L2-staged pairs
+    // -> two HBM round trips (see lift4_fused); needs an even t
+    const char *fz = std::getenv("MOA_FFT_FUSE");
+    if (t >= 24 && t % 2 == 0 && t <= 36 && !(fz && fz[0] == '0')) {
+        const int a = (t + 3) / 4, b = t / 2 - a;
+        for (int x : {a, a, b, b}) radices.push_back(int64_t(1) << x);
         return MOA_OK;
     }
     // P passes: P-1 strided passes of <= max_mid bits plus a last pass <= max_single

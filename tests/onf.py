@@ -16,12 +16,21 @@ def enumerate_pass(d):
     oo = np.zeros(nlines, np.int64)
     te = np.zeros(nlines, np.int64)
     rest = line.copy()
+    dig = np.zeros(nlines, np.int64)
     for e, si, so, st in zip(ext, d["in_str"], d["out_str"], d["tw_str"]):
         dig = rest % e
         rest //= e
         io += dig * si
         oo += dig * so
         te += dig * st
+    if d.get("ring", 0):
+        # the slowest line bits are the group; on the ring side it addresses slot (g mod slots)
+        grp = line // (nlines // d["ring_groups"])
+        slot = (grp & (d["ring_slots"] - 1)) * d["ring_G"]
+        if d["ring"] == 1:
+            io += slot
+        else:
+            oo += slot
     k = np.arange(R, dtype=np.int64)
     load = io[:, None] + k[None, :] * d["in_kstr"]
     if d["out_ksplit"] < d["logR"]:
@@ -38,8 +47,16 @@ def enumerate_pass(d):
     return load, store, tw
 
 
-def run_pass(d, src, dst):
+def group_of_lines(d):
+    ext = d["ext"]
+    nlines = int(np.prod(ext)) if ext else 1
+    return np.arange(nlines) // (nlines // d["ring_groups"])
+
+
+def run_pass(d, src, dst, lines_sel=None):
     load, store, tw = enumerate_pass(d)
+    if lines_sel is not None:
+        load, store, tw = load[lines_sel], store[lines_sel], tw[lines_sel]
     R = d["R"]
     lines = src[load]
     if not d["nodft"]:
@@ -53,8 +70,21 @@ def run_pass(d, src, dst):
 def run_plan(passes, x):
     bufs = {0: x.astype(np.complex128).copy(), 1: np.zeros(x.size, np.complex128),
             2: np.zeros(x.size, np.complex128), 3: np.zeros(x.size, np.complex128)}
-    for d in passes:
+    i = 0
+    while i < len(passes):
+        d = passes[i]
+        if d.get("ring", 0) == 2:
+            # fused pair: group by group through a ring of `slots` buffers (slot reuse exercised)
+            B = passes[i + 1]
+            ring = np.full(d["ring_slots"] * d["ring_G"], np.nan + 0j)
+            ga, gb = group_of_lines(d), group_of_lines(B)
+            for g in range(d["ring_groups"]):
+                run_pass(d, bufs[d["src"]], ring, ga == g)
+                run_pass(B, ring, bufs[B["dst"]], gb == g)
+            i += 2
+            continue
         run_pass(d, bufs[d["src"]], bufs[d["dst"]])
+        i += 1
     return bufs[1]
 
 

@@ -62,10 +62,10 @@ def test_other_argument_errors():
 def test_planner_liftings():
     assert m.moa_plan_radices(1 << 10) == [1 << 10]
     assert m.moa_plan_radices(1 << 16) == [256, 256]
-    r3 = m.moa_plan_radices(1 << 28, 1, "c128")
-    assert np.prod(r3) == 1 << 28 and len(r3) == 3 and max(r3[:-1]) <= 512
-    r4 = m.moa_plan_radices(1 << 30, 1, "c64")
-    assert np.prod(r4) == 1 << 30 and len(r4) == 3
+    assert m.moa_plan_radices(1 << 28, 1, "c128") == [128, 128, 128, 128]    # two fused pairs
+    assert m.moa_plan_radices(1 << 30, 1, "c64") == [256, 256, 128, 128]
+    r3 = m.moa_plan_radices(1 << 27, 1, "c128")                              # odd t: three passes
+    assert np.prod(r3) == 1 << 27 and len(r3) == 3 and max(r3[:-1]) <= 512
     for t in range(0, 34):
         r = m.moa_plan_radices(1 << t)
         assert int(np.prod(r)) == 1 << t and all(x <= 4096 for x in r)
@@ -146,3 +146,35 @@ def test_dist_3d_schedule_host_simulation(p):
     for r in range(p):
         want = ref[:, r * n1l:(r + 1) * n1l, :].reshape(-1)       # y-slab [k0][k1_loc][k2]
         assert np.linalg.norm(outs[r] - want) / np.linalg.norm(want) < 1e-12
+
+
+@pytest.mark.parametrize("radices,batch,dtype", [([8, 8, 8, 8], 3, "c128"), ([16, 16, 8, 8], 1, "c128"),
+                                                 ([32, 32, 16, 16], 2, "c64")])
+def test_lift4_fused_descriptors_compute_the_dft(monkeypatch, radices, batch, dtype):
+    # four-factor lifting as two L2-staged pairs (two HBM round trips)
+    monkeypatch.setenv("MOA_FFT_LIFT4", "1")
+    n = int(np.prod(radices))
+    passes = m.moa_psi_describe(n, batch, dtype, radices)
+    assert [d["ring"] for d in passes] == [2, 1, 2, 1]
+    x = synth.fill(n * batch, 16, synth.NORMAL)
+    got = run_plan(passes, x)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+    # the planner picks it for the large single transforms
+    assert [d["ring"] for d in m.moa_psi_describe(1 << 28, 1, "c128")] == [2, 1, 2, 1]
+    assert [d["ring"] for d in m.moa_psi_describe(1 << 30, 1, "c64")] == [2, 1, 2, 1]
+
+
+def test_fused_pair_descriptors_compute_the_dft():
+    # the L2-staged pass pair (ring of row buffers, slots reused) still computes the DFT
+    n, batch = 1 << 10, 100
+    passes = m.moa_psi_describe(n, batch, "c128", [32, 32])
+    assert passes[0]["ring"] == 2 and passes[1]["ring"] == 1
+    assert passes[0]["ring_groups"] == batch and passes[0]["ring_slots"] < batch
+    x = synth.fill(n * batch, 15, synth.UNIFORM)
+    got = run_plan(passes, x)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+    # cfg2's plan is one fused launch
+    p2 = m.moa_psi_describe(1 << 16, 1024, "c128")
+    assert [d["ring"] for d in p2] == [2, 1]

@@ -82,6 +82,41 @@ def test_explicit_liftings(m, torch_cuda, dtype, radices, batch):
     assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("fuse", ["1", "2", "0"])
+@pytest.mark.parametrize("n,batch,dtype,radices", [
+    (1 << 10, 100, "c128", [32, 32]), (1 << 16, 64, "c128", None), (1 << 12, 300, "c64", [64, 64]),
+    (1 << 14, 40, "c64", [128, 128]), (1 << 11, 77, "c128", [64, 32]), (1 << 20, 17, "c64", [1024, 1024]),
+])
+def test_fused_pairs(m, torch_cuda, monkeypatch, fuse, n, batch, dtype, radices):
+    # the L2-staged pass pair (ring slots reused many times; with and without the
+    # discard of consumed lines; "0" = the unfused two-launch control)
+    monkeypatch.setenv("MOA_FFT_FUSE", fuse)
+    x = synth.fill(n * batch, 21, synth.UNIFORM, dtype)
+    plan = m.FFTPlan(n, batch, dtype, radices=radices)
+    d = plan.describe()
+    assert (d[0]["ring"] == 2) == (fuse != "0")
+    for rep in range(3):                                   # epochs advance across execs
+        y = gpu_run(torch_cuda, plan, x)
+        ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+        assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype], rep
+
+
+@pytest.mark.parametrize("n,batch,dtype,radices", [
+    (1 << 12, 3, "c128", [8, 8, 8, 8]), (1 << 14, 2, "c64", [16, 16, 8, 8]), (1 << 20, 1, "c128", [64, 64, 16, 16]),
+    (1 << 24, 1, "c128", None), (1 << 24, 1, "c64", None), (1 << 26, 1, "c64", None),
+])
+def test_lift4_fused_pairs(m, torch_cuda, monkeypatch, n, batch, dtype, radices):
+    # large single transforms: four factors as two L2-staged pairs (two HBM round trips)
+    monkeypatch.setenv("MOA_FFT_LIFT4", "1")
+    x = synth.fill(n * batch, 22, synth.NORMAL, dtype)
+    plan = m.FFTPlan(n, batch, dtype, radices=radices)
+    assert [d["ring"] for d in plan.describe()] == [2, 1, 2, 1]
+    for rep in range(2):
+        y = gpu_run(torch_cuda, plan, x)
+        ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+        assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype], rep
+
+
 # ---------------------------------------------------------------- edge cases
 def test_identity_and_tiny(m, torch_cuda):
     for dtype in ("c128", "c64"):
