@@ -293,6 +293,7 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
         }
     } else {
         st = psi_3d_passes(n0, n1, n2, 1, dtype, p->passes);
+        if (!st) psi_fuse_3d(p->passes, dtype);
     }
     if (!st) st = finish_plan(p);
     if (st) {
@@ -460,6 +461,7 @@ moa_status_t moa_psi_describe_3d(int64_t n0, int64_t n1, int64_t n2, moa_dtype_t
     if (!out || !npasses) return fail(MOA_EINVAL, "describe_3d: null output");
     std::vector<moa_pass_desc_t> v;
     moa_status_t st = psi_3d_passes(n0, n1, n2, 1, dtype, v);
+    if (!st) psi_fuse_3d(v, dtype);
     if (st) return st;
     if (int(v.size()) > max_passes) return fail(MOA_EINVAL, "describe_3d: output array too small");
     for (size_t i = 0; i < v.size(); i++) out[i] = v[i];

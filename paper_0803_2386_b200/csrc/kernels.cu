@@ -109,13 +109,13 @@ template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
     }
 }
 
-// XOR swizzle inside a line: bank group = low LB bits, permuted by a Gray code
-// of the higher bits (conflict-free for the Stockham write patterns; checked
-// exhaustively on the host for R = 2^1..2^12).
-template <int LB> __device__ __forceinline__ int swz(int i) {
-    const int hi = i >> LB;
-    return i ^ ((hi ^ (hi >> 1)) & ((1 << LB) - 1));
-}
+// Shared-memory position of element i of a line: one pad element per 16, so
+// the radix-16 stride-16 writes of step 0 and the unit-stride reads are
+// bank-conflict free, and every (base + compile-time offset) folds into the
+// instruction's immediate (no per-access swizzle arithmetic).  The line stride
+// LS is chosen on the host by a conflict model of all the patterns
+// (psi_choose_tile).  LB is unused (kept for the template signature).
+template <int LB> __device__ __forceinline__ int swz(int i) { return i + (i >> 4); }
 
 struct KArgs {
     const void *in;
@@ -158,10 +158,31 @@ __device__ __forceinline__ int64_t kaddr(const KArgs &a, int k) {
     return int64_t(k & ((1 << a.ksplit) - 1)) * a.out_kstr + int64_t(k >> a.ksplit) * a.out_kstr_hi;
 }
 
-template <typename V> __device__ __forceinline__ V ld_stream(const V *p);
-template <> __device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
-template <> __device__ __forceinline__ float2 ld_stream(const float2 *p) { return __ldcs(p); }
-template <typename V> __device__ __forceinline__ void st_stream(V *p, V v) { __stcs(p, v); }
+// 128-bit / 64-bit global accesses with an L2 eviction-policy operand, so the
+// streaming HBM side (evict_first) and the L2 ring (evict_last) share one code
+// path; loads bypass L1 (.cg): ring slots are rewritten by other SMs.
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t p;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float2 ld_pol(const float2 *p, uint64_t pol) {
+    float2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_pol(double2 *p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_pol(float2 *p, float2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
 
 // One Stockham step of radix Q = 2^LQ on a line of R = 2^LR points held as
 // P = 2^LP registers per thread (thread t holds points t + m R/P).  NS = 2^LNS
@@ -201,10 +222,12 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
 template <int LR, int LP, int LB, int S, int NSTEP, typename V>
 __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int lA, int tA, int lB, int tB,
                                          const V *__restrict__ twR) {
-    constexpr int LQ0 = LR - LP * (NSTEP - 1);  // the small radix goes first (no twiddles at NS = 1)
+    // radix P for every step but the last, which takes the remainder (so step 0,
+    // whose writes are strided by its radix, always has radix 16)
+    constexpr int LQL = LR - LP * (NSTEP - 1);
     constexpr int R = 1 << LR, P = 1 << LP;
-    constexpr int LQ = S == 0 ? LQ0 : LP;
-    constexpr int LNS = S == 0 ? 0 : LQ0 + LP * (S - 1);
+    constexpr int LQ = S == NSTEP - 1 ? LQL : LP;
+    constexpr int LNS = LP * S;
     constexpr bool LAST = S == NSTEP - 1;
     if constexpr (S == 0) stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lA * LS, tA, twR);
     else stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lB * LS, tB, twR);
@@ -255,12 +278,12 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     V pts[P];
 
     // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
-    if (a.ring == 1) {
+    {
+        const uint64_t pol = l2_policy(a.ring == 1);
+        const V *base = in + io + int64_t(tA) * a.in_kstr;
+        const int64_t step = int64_t(TPL) * a.in_kstr;
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = __ldcg(in + io + int64_t(tA + m * TPL) * a.in_kstr);
-    } else {
-#pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = ld_stream(in + io + int64_t(tA + m * TPL) * a.in_kstr);
+        for (int m = 0; m < P; m++) pts[m] = ld_pol(base + m * step, pol);
     }
 
     // ---- 2. block butterflies (R-point DFT of every line); the mapping switches
@@ -315,12 +338,17 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     }
 
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
-    if (a.ring == 2) {
+    {
+        const uint64_t pol = l2_policy(a.ring == 2);
+        if (a.ksplit >= LR) {  // the common case: one affine stride per point
+            V *base = out + oo + int64_t(tB) * a.out_kstr;
+            const int64_t step = int64_t(TPL) * a.out_kstr;
 #pragma unroll
-        for (int m = 0; m < P; m++) out[oo + kaddr(a, tB + m * TPL)] = pts[m];
-    } else {
+            for (int m = 0; m < P; m++) st_pol(base + m * step, pts[m], pol);
+        } else {
 #pragma unroll
-        for (int m = 0; m < P; m++) st_stream(out + oo + kaddr(a, tB + m * TPL), pts[m]);
+            for (int m = 0; m < P; m++) st_pol(out + oo + kaddr(a, tB + m * TPL), pts[m], pol);
+        }
     }
 }
 
@@ -353,53 +381,91 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
     return v;
 }
 
-template <typename V, int LRA, int LRB>
-__global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ long long s_pos;
+// position in the tile order -> (pass B?, group, tile in group)
+__device__ __forceinline__ void decode_tile(const PairArgs &p, int64_t pos, bool &isB, int64_t &g, int64_t &idx) {
     const int64_t G = p.groups, L = p.lag, T = p.TA + p.TB;
-    if (threadIdx.x == 0) s_pos = (long long)(atomicAdd(p.qctr, 1ull) - p.epoch * (unsigned long long)(G * T));
-    __syncthreads();
-    int64_t pos = s_pos;
-    bool isB;
-    int64_t g, idx;
     const int64_t n1 = (L < G ? L : G) * p.TA;
     if (pos < n1) {
         isB = false;
         g = pos / p.TA;
         idx = pos % p.TA;
-    } else {
-        pos -= n1;
-        const int64_t n2 = G > L ? (G - L) * T : 0;
-        if (pos < n2) {
-            const int64_t s = L + pos / T, r = pos % T;
-            isB = r >= p.TA;
-            g = isB ? s - L : s;
-            idx = isB ? r - p.TA : r;
-        } else {
-            pos -= n2;
-            isB = true;
-            g = (G > L ? G - L : 0) + pos / p.TB;
-            idx = pos % p.TB;
-        }
+        return;
     }
-    if (threadIdx.x == 0) {
-        const unsigned long long round = p.epoch + 1;
-        if (isB) {
-            while (ld_acquire(p.cntA + g) < round * (unsigned long long)p.TA) __nanosleep(100);
-        } else if (g > p.slot_mask) {
-            while (ld_acquire(p.cntB + g - (p.slot_mask + 1)) < round * (unsigned long long)p.TB) __nanosleep(100);
-        }
+    pos -= n1;
+    const int64_t n2 = G > L ? (G - L) * T : 0;
+    if (pos < n2) {
+        const int64_t s = L + pos / T, r = pos % T;
+        isB = r >= p.TA;
+        g = isB ? s - L : s;
+        idx = isB ? r - p.TA : r;
+        return;
     }
+    pos -= n2;
+    isB = true;
+    g = (G > L ? G - L : 0) + pos / p.TB;
+    idx = pos % p.TB;
+}
+
+// Persistent CTAs (grid = resident capacity): each loops over the tile queue,
+// fetching its next tile index while it works on the current one, so the
+// queue atomic's latency is hidden.
+template <typename V, int LRA, int LRB>
+__global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ long long s_next;
+    __shared__ KArgs s_args;
+    const int64_t total = p.groups * (p.TA + p.TB);
+    // the queue counter is zeroed before every launch (each CTA's last fetch
+    // overshoots the end, so an epoch-based base would drift); the per-group
+    // completion counters only ever grow, by exactly TA / TB per launch
+    const unsigned long long base = 0;
+    const unsigned long long round = p.epoch + 1;
+    if (threadIdx.x == 0) s_next = (long long)(atomicAdd(p.qctr, 1ull) - base);
     __syncthreads();
-    const int64_t ring_off = (g & p.slot_mask) * p.ringG;
+    int64_t pos = s_next;
     V *sm = reinterpret_cast<V *>(smem_raw);
-    if (isB) tile_body<V, LRB>(p.B, (g * p.TB + idx) * p.B.W, sm, ring_off);
-    else tile_body<V, LRA>(p.A, (g * p.TA + idx) * p.A.W, sm, ring_off);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(isB ? p.cntB + g : p.cntA + g, 1ull);
+    while (pos < total) {
+        bool isB;
+        int64_t g, idx;
+        decode_tile(p, pos, isB, g, idx);
+        __syncthreads();  // everyone has read s_next / finished the previous tile
+        if (threadIdx.x == 0) {
+            // (a watchdog turns a broken schedule into a launch error instead of a hang)
+            unsigned spins = 0;
+            if (isB) {
+                while (ld_acquire(p.cntA + g) < round * (unsigned long long)p.TA) {
+                    __nanosleep(64);
+                    if (++spins > (1u << 26)) __trap();
+                }
+            } else if (g > p.slot_mask) {
+                while (ld_acquire(p.cntB + g - (p.slot_mask + 1)) < round * (unsigned long long)p.TB) {
+                    __nanosleep(64);
+                    if (++spins > (1u << 26)) __trap();
+                }
+            }
+            s_next = (long long)(atomicAdd(p.qctr, 1ull) - base);
+        }
+        const int64_t ring_off = (g & p.slot_mask) * p.ringG;
+        if constexpr (LRA == LRB) {
+            // one inlined tile body for both passes (the fused kernel otherwise
+            // thrashes the instruction cache); the pass's arguments are staged in
+            // shared memory
+            constexpr int NW = sizeof(KArgs) / 4;
+            const int *src = reinterpret_cast<const int *>(isB ? &p.B : &p.A);
+            for (int i = threadIdx.x; i < NW; i += blockDim.x) reinterpret_cast<int *>(&s_args)[i] = src[i];
+            __syncthreads();
+            tile_body<V, LRA>(s_args, (g * (isB ? p.TB : p.TA) + idx) * s_args.W, sm, ring_off);
+        } else {
+            __syncthreads();
+            if (isB) tile_body<V, LRB>(p.B, (g * p.TB + idx) * p.B.W, sm, ring_off);
+            else tile_body<V, LRA>(p.A, (g * p.TA + idx) * p.A.W, sm, ring_off);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(isB ? p.cntB + g : p.cntA + g, 1ull);
+        }
+        pos = s_next;
     }
 }
 
@@ -493,7 +559,17 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
         if (e != cudaSuccess) return e;
     }
     const int64_t tiles = p.groups * (p.TA + p.TB);
-    fn<<<dim3(unsigned(tiles)), dim3(unsigned(dA.threads)), size_t(smem), stream>>>(p);
+    // persistent grid: every CTA resident at once (required by the waits)
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, dA.threads, smem);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = int64_t(per_sm > 0 ? per_sm : 1) * sms;
+    if (grid > tiles) grid = tiles;
+    e = cudaMemsetAsync(rs.qctr, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    fn<<<dim3(unsigned(grid)), dim3(unsigned(dA.threads)), size_t(smem), stream>>>(p);
     return cudaGetLastError();
 }
 }  // namespace

@@ -57,6 +57,8 @@ cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, mo
 // group working set fits (marks ring fields; returns how many pairs were made)
 int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,
                    moa_dtype_t dtype);
+// 3-D: fuse the z- and y-passes (group = one x-plane)
+int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype);
 // The descriptors a 1-D plan runs: a planned 4-factor lifting (or any
 // 4-factor lifting with MOA_FFT_LIFT4=1) as two fused pairs, otherwise the
 // plain passes with the 2-pass fusion where it applies.

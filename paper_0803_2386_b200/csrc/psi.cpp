@@ -53,6 +53,7 @@ static void add_digit(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, i
 }
 
 static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W);
+int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total);
 
 void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int esize = dtype == MOA_C128 ? 16 : 8;
@@ -87,12 +88,108 @@ static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
     const bool lf = d.lf_load || d.lf_store;
     d.W = int32_t(W);
     d.threads = int32_t(W * TPL);
-    int64_t pad;
-    if (TPL >= slots) pad = lf ? (W >= slots ? 1 : slots / W) : 1;
-    else pad = TPL;
-    d.line_pad = int32_t(pad);
+    // shared-memory line stride: the kernel stores element i of line l at
+    // l*LS + i + i/16; pick LS (>= R + R/16) with the fewest bank conflicts over
+    // every access pattern of this tile (exchange writes/reads of each step in
+    // its thread mapping), evaluated exactly on the first warps
+    (void)slots;
+    const int64_t base = R + R / 16;
+    int64_t best = base, best_w = 1 << 30, best_t = int64_t(1) << 62;
+    for (int64_t LS = base; LS < base + 2 * (128 / esize); LS++) {
+        int64_t tot = 0;
+        const int w = psi_bank_conflicts(logR, W, esize, d.lf_load, d.lf_store, LS, &tot);
+        if (w < best_w || (w == best_w && tot < best_t)) {
+            best = LS;
+            best_w = w;
+            best_t = tot;
+        }
+    }
+    d.line_pad = int32_t(best - R);
     const bool needs_smem = lf || logR > logP;
-    d.smem_bytes = needs_smem ? int32_t(W * (R + pad) * esize) : 0;
+    d.smem_bytes = needs_smem ? int32_t(W * best * esize) : 0;
+}
+
+// Worst-case conflict degree (and total extra wavefronts) of the shared-memory
+// accesses a pass tile makes, mirroring kernels.cu: Stockham step s has radix
+// 16 except the last (the remainder), NS = 16^s, group j = t + u R/P writes
+// element (j/NS) NS Q + j%NS + r NS; the next step reads t + m R/P.  Thread
+// mapping: step 0 in the load side's, later steps in the store side's
+// (line-fast: l = tid % W, t = tid / W; point-fast: l = tid / TPL, t = tid % TPL).
+int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total) {
+    const int logP = logR < 4 ? logR : 4;
+    const int64_t R = int64_t(1) << logR, P = int64_t(1) << logP, TPL = R / P, nthr = W * TPL;
+    const int per = 128 / esize;  // lanes per shared-memory wavefront
+    const int nstep = logR == 0 ? 1 : (logR + logP - 1) / logP;
+    const int lql = logR - logP * (nstep - 1);
+    auto phys = [](int64_t i) { return i + (i >> 4); };
+    auto map = [&](int64_t tid, bool lf, int64_t &l, int64_t &t) {
+        if (lf) { l = tid % W; t = tid / W; }
+        else { l = tid / TPL; t = tid % TPL; }
+    };
+    int worst = 1;
+    int64_t tot = 0;
+    auto eval = [&](auto addr) {  // addr(tid) -> element address or -1
+        for (int64_t w0 = 0; w0 < nthr && w0 < 256; w0 += 32)
+            for (int ph = 0; ph < 32; ph += per) {
+                int64_t seen[32];
+                int ns = 0, deg[32] = {0};
+                int64_t bank[32];
+                for (int ln = ph; ln < ph + per; ln++) {
+                    const int64_t tid = w0 + ln;
+                    if (tid >= nthr) continue;
+                    const int64_t a = addr(tid);
+                    bool dup = false;
+                    for (int k = 0; k < ns; k++) dup |= seen[k] == a;
+                    if (dup) continue;
+                    seen[ns] = a;
+                    bank[ns] = a % per;
+                    ns++;
+                }
+                int dmax = 1;
+                for (int k = 0; k < ns; k++) {
+                    int c = 0;
+                    for (int q = 0; q < ns; q++) c += bank[q] == bank[k];
+                    deg[k] = c;
+                    if (c > dmax) dmax = c;
+                }
+                if (dmax > worst) worst = dmax;
+                tot += dmax - 1;
+            }
+    };
+    for (int s = 0; s < nstep - 1; s++) {
+        const int64_t Q = int64_t(1) << (s == nstep - 1 ? lql : logP), NS = int64_t(1) << (logP * s), G = P / Q;
+        const bool lf = s == 0 ? lfA : lfB;
+        for (int64_t u = 0; u < G; u++)
+            for (int64_t r = 0; r < Q; r++)
+                eval([&](int64_t tid) {
+                    int64_t l, t;
+                    map(tid, lf, l, t);
+                    const int64_t j = t + u * (R / P);
+                    return l * LS + phys((j / NS) * NS * Q + (j % NS) + r * NS);
+                });
+        for (int64_t mm = 0; mm < P; mm++)
+            eval([&](int64_t tid) {
+                int64_t l, t;
+                map(tid, lfB, l, t);
+                return l * LS + phys(t + mm * TPL);
+            });
+    }
+    if (nstep == 1 && lfA != lfB) {
+        for (int64_t mm = 0; mm < P; mm++) {
+            eval([&](int64_t tid) {
+                int64_t l, t;
+                map(tid, lfA, l, t);
+                return l * LS + phys(t + mm * TPL);
+            });
+            eval([&](int64_t tid) {
+                int64_t l, t;
+                map(tid, lfB, l, t);
+                return l * LS + phys(t + mm * TPL);
+            });
+        }
+    }
+    if (total) *total = tot;
+    return worst;
 }
 
 moa_status_t psi_lift_passes(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
@@ -227,17 +324,24 @@ moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, 
 // strided columns j of row b) and pass B's lines (the rows k_0 of row b) both
 // have the row b as their last (slowest) digit; on the ring side that digit's
 // stride becomes (b mod slots) * n.
-int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,
-                   moa_dtype_t dtype) {
+// Fuse passes[i] and passes[i+1] into an L2-staged pair when (a) both have the
+// same slowest line digit -- the group -- with one stride G on the
+// intermediate's side (A's store, B's load), (b) a group (G elements) fits the
+// ring budget a few times over, (c) the CTA sizes can be equalised.
+static int fuse_two(std::vector<moa_pass_desc_t> &passes, size_t i, moa_dtype_t dtype, int64_t min_groups,
+                    int64_t ring_budget) {
     const char *env = std::getenv("MOA_FFT_FUSE");
     if (env && env[0] == '0') return 0;
+    if (i + 1 >= passes.size()) return 0;
     const int64_t esize = dtype == MOA_C128 ? 16 : 8;
-    if (passes.size() != 2 || radices.size() != 2) return 0;
-    moa_pass_desc_t &A = passes[0], &B = passes[1];
-    const int64_t gbytes = n * esize;
-    if (batch < 16 || gbytes > (int64_t(8) << 20)) return 0;
+    moa_pass_desc_t &A = passes[i], &B = passes[i + 1];
+    if (A.ring || B.ring || A.ndig < 2 || B.ndig < 2) return 0;
+    const int la = A.ndig - 1, lb = B.ndig - 1;
+    const int64_t groups = A.ext[la], G = A.out_str[la];
+    if (B.ext[lb] != groups || B.in_str[lb] != G || groups < min_groups) return 0;
+    if (A.dst != B.src || A.dst < 0) return 0;
+    if (G * esize * 4 > ring_budget) return 0;
     if (A.logR < 5 || A.logR > 10 || B.logR < 5 || B.logR > 10) return 0;
-    if (A.ndig != 2 || B.ndig != 2) return 0;
     if (A.threads != B.threads) {  // equalise the CTA size by widening the narrower tile
         moa_pass_desc_t &lo = A.threads < B.threads ? A : B;
         const moa_pass_desc_t &hi = A.threads < B.threads ? B : A;
@@ -246,24 +350,40 @@ int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64
         set_tile(lo, dtype, W);
         if (A.threads != B.threads) return 0;
     }
-    if (A.ext[1] != batch || B.ext[1] != batch) return 0;
     int64_t slots = 4;
-    while (slots * 2 * gbytes <= (int64_t(32) << 20) && slots < 64) slots *= 2;
+    while (slots * 2 * G * esize <= ring_budget && slots < 64) slots *= 2;
     for (moa_pass_desc_t *d : {&A, &B}) {
         d->ring_slots = int32_t(slots);
         d->ring_lag = int32_t(slots / 2);
-        d->ring_discard = 1;
-        d->ring_groups = batch;
-        d->ring_G = n;
+        d->ring_discard = !(env && env[0] == '2');
+        d->ring_groups = groups;
+        d->ring_G = G;
     }
     A.ring = 2;
-    A.out_str[1] = 0;  // the group digit addresses the ring slot
+    A.out_str[la] = 0;  // the group digit addresses the ring slot
     A.dst = -1;
     B.ring = 1;
-    B.in_str[1] = 0;
+    B.in_str[lb] = 0;
     B.src = -1;
-    if (env && env[0] == '2') A.ring_discard = B.ring_discard = 0;
     return 1;
+}
+
+// L2-level lifting: a two-pass lifting of many independent
+// rows (the cfg2 shape) becomes one fused pass pair whose intermediate lives in
+// an L2-resident ring of row buffers (group = one row).
+int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,
+                   moa_dtype_t dtype) {
+    (void)n;
+    (void)batch;
+    if (passes.size() != 2 || radices.size() != 2) return 0;
+    return fuse_two(passes, 0, dtype, 16, int64_t(32) << 20);
+}
+
+// 3-D: the z- and y-passes of one x-plane form a group (the plane), so the
+// pair costs one HBM round trip instead of two.
+int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
+    if (passes.size() != 3) return 0;
+    return fuse_two(passes, 0, dtype, 8, int64_t(64) << 20);
 }
 
 // Four-pass lifting n = R0 R1 R2 R3 run as two L2-staged pairs, so a single
@@ -286,6 +406,8 @@ static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, con
     const int64_t R0 = R[0], R1 = R[1], R2 = R[2], R3 = R[3];
     const int64_t S1 = R2 * R3, S0 = R1 * S1, N1 = S0, N2 = S1;
     if (R0 < W || S1 < W || R3 < W) return fail(MOA_EUNSUPPORTED, "psi: lift4 needs R0, R3 >= W");
+    for (int i = 0; i < 4; i++)
+        if (R[i] < 32 || R[i] > 1024) return fail(MOA_EUNSUPPORTED, "psi: lift4 radices must be in [32, 1024]");
     const int64_t G01 = R0 * R1 * W, G23 = W * R2 * R3;
     const int64_t g01 = (S1 / W) * batch, g23 = R1 * (R0 / W) * batch;
     auto ring = [&](moa_pass_desc_t &d, int side, int64_t groups, int64_t G) {

@@ -53,8 +53,8 @@ def group_of_lines(d):
     return np.arange(nlines) // (nlines // d["ring_groups"])
 
 
-def run_pass(d, src, dst, lines_sel=None):
-    load, store, tw = enumerate_pass(d)
+def run_pass(d, src, dst, lines_sel=None, enum=None):
+    load, store, tw = enumerate_pass(d) if enum is None else enum
     if lines_sel is not None:
         load, store, tw = load[lines_sel], store[lines_sel], tw[lines_sel]
     R = d["R"]
@@ -77,10 +77,11 @@ def run_plan(passes, x):
             # fused pair: group by group through a ring of `slots` buffers (slot reuse exercised)
             B = passes[i + 1]
             ring = np.full(d["ring_slots"] * d["ring_G"], np.nan + 0j)
-            ga, gb = group_of_lines(d), group_of_lines(B)
-            for g in range(d["ring_groups"]):
-                run_pass(d, bufs[d["src"]], ring, ga == g)
-                run_pass(B, ring, bufs[B["dst"]], gb == g)
+            ea, eb = enumerate_pass(d), enumerate_pass(B)
+            la, lb = len(ea[0]) // d["ring_groups"], len(eb[0]) // B["ring_groups"]
+            for g in range(d["ring_groups"]):          # lines of a group are contiguous in ONF order
+                run_pass(d, bufs[d["src"]], ring, slice(g * la, (g + 1) * la), ea)
+                run_pass(B, ring, bufs[B["dst"]], slice(g * lb, (g + 1) * lb), eb)
             i += 2
             continue
         run_pass(d, bufs[d["src"]], bufs[d["dst"]])
