@@ -47,6 +47,8 @@ struct moa_fft_plan_s {
     void *staging = nullptr;
     DistPlan *dist = nullptr;  // processor-level lifting (comm.cpp)
     std::vector<RingState> rings;  // rings[i] valid where passes[i].ring == 2
+    moa_fft_plan_s *sub[2] = {nullptr, nullptr};  // exec_host chunk pipeline (rows / 8 each)
+    cudaStream_t ss[2] = {nullptr, nullptr};
     // per-step event profiling (moa_fft_prof_begin / _end)
     std::vector<cudaEvent_t> prof_ev;
     int prof_max = 0, prof_count = 0, prof_nsteps = 0;
@@ -355,7 +357,44 @@ moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host
         if (st) return st;
     }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemcpyAsync(p->staging, host_in, bytes, cudaMemcpyHostToDevice, s);
+    cudaError_t e;
+    // Independent rows: pipeline chunks of rows over two streams so the
+    // host->device copy of chunk c+1, the FFT of chunk c and the device->host
+    // copy of chunk c-1 overlap (PCIe is full duplex).  Each stream has its own
+    // sub-plan (plans are not re-entrant) and its own half of the staging buffer.
+    const int64_t nch = (!p->dist && !p->is3d && p->batch >= 8) ? 8 : 1;
+    if (nch > 1 && p->batch % nch == 0) {
+        const int64_t rows = p->batch / nch;
+        const size_t cb = size_t(rows * p->n) * p->esize;
+        if (!p->sub[0]) {
+            for (int k = 0; k < 2; k++) {
+                moa_status_t st = moa_fft_plan(&p->sub[k], p->n, rows, p->dtype, 1);
+                if (st) return st;
+                e = cudaStreamCreateWithFlags(&p->ss[k], cudaStreamNonBlocking);
+                if (e != cudaSuccess) return cuda_fail(e, "exec_host stream");
+            }
+        }
+        e = cudaStreamSynchronize(s);  // the caller's prior work on its stream is done
+        if (e != cudaSuccess) return cuda_fail(e, "exec_host sync");
+        for (int64_t c = 0; c < nch; c++) {
+            const int k = int(c & 1);
+            char *stg = static_cast<char *>(p->staging) + size_t(k) * cb;  // two chunk buffers
+            e = cudaMemcpyAsync(stg, static_cast<const char *>(host_in) + size_t(c) * cb, cb, cudaMemcpyHostToDevice,
+                                p->ss[k]);
+            if (e != cudaSuccess) return cuda_fail(e, "exec_host H2D");
+            moa_status_t st = moa_fft_exec(p->sub[k], stg, stg, p->ss[k]);
+            if (st) return st;
+            e = cudaMemcpyAsync(static_cast<char *>(host_out) + size_t(c) * cb, stg, cb, cudaMemcpyDeviceToHost,
+                                p->ss[k]);
+            if (e != cudaSuccess) return cuda_fail(e, "exec_host D2H");
+        }
+        for (int k = 0; k < 2; k++) {
+            e = cudaStreamSynchronize(p->ss[k]);
+            if (e != cudaSuccess) return cuda_fail(e, "exec_host sync");
+        }
+        return MOA_OK;
+    }
+    e = cudaMemcpyAsync(p->staging, host_in, bytes, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "exec_host H2D");
     moa_status_t st = moa_fft_exec(p, p->staging, p->staging, stream);
     if (st) return st;
@@ -424,6 +463,10 @@ moa_status_t moa_fft_prof_end(moa_fft_plan_t p, double *step_ms, int max_steps, 
 moa_status_t moa_fft_destroy(moa_fft_plan_t p) {
     if (!p) return MOA_OK;
     prof_free(p);
+    for (int k = 0; k < 2; k++) {
+        if (p->sub[k]) moa_fft_destroy(p->sub[k]);
+        if (p->ss[k]) cudaStreamDestroy(p->ss[k]);
+    }
     for (void *a : p->allocs) cudaFree(a);
     if (p->dist) dist_plan_free(p->dist);
     delete p;

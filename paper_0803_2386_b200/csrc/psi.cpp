@@ -65,7 +65,9 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // Lines per tile: enough adjacent lines for full 128-byte runs on a
     // line-coalesced side; enough threads per CTA otherwise.
     int64_t W = lf ? slots : (TPL >= 256 ? 1 : 256 / TPL);
-    const int64_t smem_cap = 100 * 1024;  // two CTAs per SM
+    // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
+    const char *cap_env = std::getenv("MOA_FFT_SMEM_CAP");
+    const int64_t smem_cap = cap_env ? std::atoll(cap_env) : 100 * 1024;
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
@@ -350,8 +352,10 @@ static int fuse_two(std::vector<moa_pass_desc_t> &passes, size_t i, moa_dtype_t 
         set_tile(lo, dtype, W);
         if (A.threads != B.threads) return 0;
     }
+    const char *mb = std::getenv("MOA_FFT_RING_MB");  // ablation: ring size budget
+    if (mb) ring_budget = std::atoll(mb) << 20;
     int64_t slots = 4;
-    while (slots * 2 * G * esize <= ring_budget && slots < 64) slots *= 2;
+    while (slots * 2 * G * esize <= ring_budget && slots < 128 && slots * 4 <= groups) slots *= 2;
     for (moa_pass_desc_t *d : {&A, &B}) {
         d->ring_slots = int32_t(slots);
         d->ring_lag = int32_t(slots / 2);
