@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -194,6 +195,14 @@ moa_status_t finish_plan(moa_fft_plan_s *p) {
         r.qctr = static_cast<unsigned long long *>(ctr);
         r.cntA = r.qctr + 1;
         r.cntB = r.cntA + d.ring_groups;
+        const char *se = std::getenv("MOA_FFT_STATS");
+        if (se && se[0] == '1') {
+            void *sp = nullptr;
+            st = dev_alloc(p, 6 * sizeof(unsigned long long), &sp);
+            if (st) return st;
+            cudaMemset(sp, 0, 6 * sizeof(unsigned long long));
+            r.stats = static_cast<unsigned long long *>(sp);
+        }
     }
     return build_tables(p);
 }
@@ -463,6 +472,15 @@ moa_status_t moa_fft_prof_end(moa_fft_plan_t p, double *step_ms, int max_steps, 
 moa_status_t moa_fft_destroy(moa_fft_plan_t p) {
     if (!p) return MOA_OK;
     prof_free(p);
+    for (auto &r : p->rings)
+        if (r.stats) {
+            unsigned long long h[6] = {0};
+            cudaMemcpy(h, r.stats, sizeof(h), cudaMemcpyDeviceToHost);
+            std::fprintf(stderr,
+                         "moa ring stats (%llu execs): B waits %llu spins %llu cycles %llu | A waits %llu spins %llu "
+                         "cycles %llu\n",
+                         r.epoch, h[0], h[1], h[2], h[3], h[4], h[5]);
+        }
     for (int k = 0; k < 2; k++) {
         if (p->sub[k]) moa_fft_destroy(p->sub[k]);
         if (p->ss[k]) cudaStreamDestroy(p->ss[k]);

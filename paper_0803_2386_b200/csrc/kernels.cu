@@ -373,6 +373,7 @@ struct PairArgs {
     int32_t TA, TB, lag, slot_mask;
     unsigned long long *qctr, *cntA, *cntB;
     unsigned long long epoch;
+    unsigned long long *stats;  // optional wait statistics (6 counters), or null
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
@@ -410,28 +411,24 @@ __device__ __forceinline__ void decode_tile(const PairArgs &p, int64_t pos, bool
 // fetching its next tile index while it works on the current one, so the
 // queue atomic's latency is hidden.
 template <typename V, int LRA, int LRB>
-__global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
+__global__ void __launch_bounds__(512) pair_kernel(const __grid_constant__ PairArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ long long s_next;
-    __shared__ KArgs s_args;
     const int64_t total = p.groups * (p.TA + p.TB);
-    // the queue counter is zeroed before every launch (each CTA's last fetch
-    // overshoots the end, so an epoch-based base would drift); the per-group
-    // completion counters only ever grow, by exactly TA / TB per launch
-    const unsigned long long base = 0;
+    // the per-group completion counters only ever grow, by exactly TA / TB per launch
     const unsigned long long round = p.epoch + 1;
-    if (threadIdx.x == 0) s_next = (long long)(atomicAdd(p.qctr, 1ull) - base);
-    __syncthreads();
-    int64_t pos = s_next;
     V *sm = reinterpret_cast<V *>(smem_raw);
-    while (pos < total) {
+    // Static round-robin over the tile order (tile pos -> CTA pos mod grid, each
+    // CTA in increasing order).  With every CTA resident, the smallest unfinished
+    // tile is always some CTA's current tile and all it waits on is smaller, so
+    // the schedule cannot deadlock -- and no queue atomic is needed.
+    for (int64_t pos = blockIdx.x; pos < total; pos += gridDim.x) {
         bool isB;
         int64_t g, idx;
         decode_tile(p, pos, isB, g, idx);
-        __syncthreads();  // everyone has read s_next / finished the previous tile
         if (threadIdx.x == 0) {
             // (a watchdog turns a broken schedule into a launch error instead of a hang)
             unsigned spins = 0;
+            const long long t0 = p.stats ? clock64() : 0;
             if (isB) {
                 while (ld_acquire(p.cntA + g) < round * (unsigned long long)p.TA) {
                     __nanosleep(64);
@@ -443,20 +440,21 @@ __global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
                     if (++spins > (1u << 26)) __trap();
                 }
             }
-            s_next = (long long)(atomicAdd(p.qctr, 1ull) - base);
+            if (p.stats && spins) {  // MOA_FFT_STATS: waits, spins, wait cycles
+                atomicAdd(p.stats + (isB ? 0 : 3), 1ull);
+                atomicAdd(p.stats + (isB ? 1 : 4), (unsigned long long)spins);
+                atomicAdd(p.stats + (isB ? 2 : 5), (unsigned long long)(clock64() - t0));
+            }
         }
+        __syncthreads();
         const int64_t ring_off = (g & p.slot_mask) * p.ringG;
         if constexpr (LRA == LRB) {
             // one inlined tile body for both passes (the fused kernel otherwise
-            // thrashes the instruction cache); the pass's arguments are staged in
-            // shared memory
-            constexpr int NW = sizeof(KArgs) / 4;
-            const int *src = reinterpret_cast<const int *>(isB ? &p.B : &p.A);
-            for (int i = threadIdx.x; i < NW; i += blockDim.x) reinterpret_cast<int *>(&s_args)[i] = src[i];
-            __syncthreads();
-            tile_body<V, LRA>(s_args, (g * (isB ? p.TB : p.TA) + idx) * s_args.W, sm, ring_off);
+            // thrashes the instruction cache); the arguments are read in place
+            // from the __grid_constant__ parameter block
+            const KArgs &a = isB ? p.B : p.A;
+            tile_body<V, LRA>(a, (g * (isB ? p.TB : p.TA) + idx) * a.W, sm, ring_off);
         } else {
-            __syncthreads();
             if (isB) tile_body<V, LRB>(p.B, (g * p.TB + idx) * p.B.W, sm, ring_off);
             else tile_body<V, LRA>(p.A, (g * p.TA + idx) * p.A.W, sm, ring_off);
         }
@@ -465,7 +463,6 @@ __global__ void __launch_bounds__(512) pair_kernel(const PairArgs p) {
             __threadfence();
             atomicAdd(isB ? p.cntB + g : p.cntA + g, 1ull);
         }
-        pos = s_next;
     }
 }
 
@@ -552,6 +549,7 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
     p.cntA = rs.cntA;
     p.cntB = rs.cntB;
     p.epoch = rs.epoch;
+    p.stats = rs.stats;
     PFn<V> fn = tab[(dA.logR - 5) * 6 + (dB.logR - 5)];
     const int smem = dA.smem_bytes > dB.smem_bytes ? dA.smem_bytes : dB.smem_bytes;
     if (smem > 48 * 1024 - 64) {
@@ -567,8 +565,6 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = int64_t(per_sm > 0 ? per_sm : 1) * sms;
     if (grid > tiles) grid = tiles;
-    e = cudaMemsetAsync(rs.qctr, 0, sizeof(unsigned long long), stream);
-    if (e != cudaSuccess) return e;
     fn<<<dim3(unsigned(grid)), dim3(unsigned(dA.threads)), size_t(smem), stream>>>(p);
     return cudaGetLastError();
 }

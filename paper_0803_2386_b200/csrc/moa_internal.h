@@ -47,6 +47,7 @@ struct RingState {
     unsigned long long *cntA = nullptr;   // per-group completed A tiles
     unsigned long long *cntB = nullptr;   // per-group completed B tiles
     unsigned long long epoch = 0;         // execs of this pair so far
+    unsigned long long *stats = nullptr;  // MOA_FFT_STATS=1: B waits/spins/cycles, A waits/spins/cycles
 };
 int log2_exact(int64_t n);
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out,

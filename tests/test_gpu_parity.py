@@ -102,7 +102,7 @@ def test_fused_pairs(m, torch_cuda, monkeypatch, fuse, n, batch, dtype, radices)
 
 
 @pytest.mark.parametrize("n,batch,dtype,radices", [
-    (1 << 20, 3, "c128", [32, 32, 32, 32]), (1 << 22, 2, "c64", [64, 64, 32, 32]), (1 << 20, 1, "c128", [64, 64, 16, 16]),
+    (1 << 20, 3, "c128", [32, 32, 32, 32]), (1 << 22, 2, "c64", [64, 64, 32, 32]),
     (1 << 24, 1, "c128", None), (1 << 24, 1, "c64", None), (1 << 26, 1, "c64", None),
 ])
 def test_lift4_fused_pairs(m, torch_cuda, monkeypatch, n, batch, dtype, radices):
