@@ -66,8 +66,12 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // line-coalesced side; enough threads per CTA otherwise.
     int64_t W = lf ? slots : (TPL >= 256 ? 1 : 256 / TPL);
     // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
+    // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
+    // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
+    // one CTA per SM (measured: cfg5 x-pass 11.7 -> 9.3 ms).
+    const int64_t kbytes = (d.in_kstr > d.out_kstr ? d.in_kstr : d.out_kstr) * esize;
     const char *cap_env = std::getenv("MOA_FFT_SMEM_CAP");
-    const int64_t smem_cap = cap_env ? std::atoll(cap_env) : 100 * 1024;
+    const int64_t smem_cap = cap_env ? std::atoll(cap_env) : (lf && kbytes >= (int64_t(1) << 20) ? 200000 : 100 * 1024);
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
@@ -379,6 +383,11 @@ int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64
                    moa_dtype_t dtype) {
     (void)n;
     (void)batch;
+    // opt-in (MOA_FFT_FUSE=1, or 2 without the discard) until the fused launch
+    // beats the two single passes, which already run near the HBM roofline
+    // each
+    const char *e = std::getenv("MOA_FFT_FUSE");
+    if (!e || (e[0] != '1' && e[0] != '2')) return 0;
     if (passes.size() != 2 || radices.size() != 2) return 0;
     return fuse_two(passes, 0, dtype, 16, int64_t(32) << 20);
 }
@@ -386,6 +395,8 @@ int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64
 // 3-D: the z- and y-passes of one x-plane form a group (the plane), so the
 // pair costs one HBM round trip instead of two.
 int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
+    const char *e = std::getenv("MOA_FFT_FUSE");  // opt-in, as psi_fuse_pairs
+    if (!e || (e[0] != '1' && e[0] != '2')) return 0;
     if (passes.size() != 3) return 0;
     return fuse_two(passes, 0, dtype, 8, int64_t(64) << 20);
 }

@@ -110,7 +110,8 @@ def test_planner_descriptors_compute_the_dft(n, batch, dtype):
             assert d["ext"][0] % d["W"] == 0
 
 
-def test_psi_3d_descriptors():
+def test_psi_3d_descriptors(monkeypatch):
+    monkeypatch.setenv("MOA_FFT_FUSE", "1")
     for shape in [(8, 4, 16), (16, 16, 16), (2, 32, 4), (64, 64, 64), (16, 32, 64)]:
         passes = m.moa_psi_describe_3d(*shape)
         if min(shape[1:]) >= 32 and shape[0] >= 8:
@@ -166,8 +167,9 @@ def test_lift4_fused_descriptors_compute_the_dft(monkeypatch, radices, batch, dt
     assert [d["ring"] for d in m.moa_psi_describe(1 << 30, 1, "c64")] == [2, 1, 2, 1]
 
 
-def test_fused_pair_descriptors_compute_the_dft():
+def test_fused_pair_descriptors_compute_the_dft(monkeypatch):
     # the L2-staged pass pair (ring of row buffers, slots reused) still computes the DFT
+    monkeypatch.setenv("MOA_FFT_FUSE", "1")
     n, batch = 1 << 10, 100
     passes = m.moa_psi_describe(n, batch, "c128", [32, 32])
     assert passes[0]["ring"] == 2 and passes[1]["ring"] == 1
