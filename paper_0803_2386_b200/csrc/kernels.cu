@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include <array>
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 
@@ -250,41 +251,38 @@ __device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, con
     return cmul(__ldg(hi + (e >> h)), __ldg(lo + (e & ((int64_t(1) << h) - 1))));
 }
 
-// One tile (W adjacent lines starting at line0) of a pass.  ring >= 0: the
-// ring slot of this tile's group (the L2-staged intermediate of a fused pass
-// pair, see pair_kernel); the ring side's address gets slot * ringG added.
+// Thread mappings of a tile.  Point-fast: lanes over the points of one line (a
+// side whose points are contiguous).  Line-fast: lanes over the W adjacent
+// lines (a strided side: each warp request covers whole 128-byte runs).  A is
+// the load side's mapping, B the store side's.
+struct TileMap {
+    int lA, tA, lB, tB;
+};
+template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
+    const int tid = threadIdx.x;
+    TileMap m;
+    m.lA = a.lf_load ? tid % a.W : tid / TPL;
+    m.tA = a.lf_load ? tid / a.W : tid % TPL;
+    m.lB = a.lf_store ? tid % a.W : tid / TPL;
+    m.tB = a.lf_store ? tid / a.W : tid % TPL;
+    return m;
+}
+
+// The rest of a tile once its points are in registers (mapping A): block
+// butterflies, lifted weights, store.  ring >= 0: the ring slot of this
+// tile's group (the L2-staged intermediate of a fused pass pair, see
+// pair_kernel); the ring side's address gets slot * ringG added.
 template <typename V, int LR>
-__device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
+__device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
+                                             V (&pts)[1 << (LR < 4 ? LR : 4)]) {
     constexpr int LP = LR < 4 ? LR : 4;
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
     constexpr int NSTEP = LR == 0 ? 1 : (LR + LP - 1) / LP;
-    const V *__restrict__ in = reinterpret_cast<const V *>(a.in);
     V *__restrict__ out = reinterpret_cast<V *>(a.out);
     const V *__restrict__ twR = reinterpret_cast<const V *>(a.twR);
-
-    const int tid = threadIdx.x;
-    // Thread mappings.  Point-fast: lanes over the points of one line (a side
-    // whose points are contiguous).  Line-fast: lanes over the W adjacent lines
-    // (a strided side: each warp request covers whole 128-byte runs).  A uses
-    // the load side's mapping, B the store side's.
-    const int lA = a.lf_load ? tid % a.W : tid / TPL, tA = a.lf_load ? tid / a.W : tid % TPL;
-    const int lB = a.lf_store ? tid % a.W : tid / TPL, tB = a.lf_store ? tid / a.W : tid % TPL;
-    int64_t io, oo, te, unused0, unused1;
-    line_offsets(a, line0 + lA, io, unused0, unused1);
-    line_offsets(a, line0 + lB, unused0, oo, te);
-    if (a.ring == 1) io += ring_off;
-    if (a.ring == 2) oo += ring_off;
-    V pts[P];
-
-    // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
-    {
-        const uint64_t pol = l2_policy(a.ring == 1);
-        const V *base = in + io + int64_t(tA) * a.in_kstr;
-        const int64_t step = int64_t(TPL) * a.in_kstr;
-#pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = ld_pol(base + m * step, pol);
-    }
+    const TileMap mp = tile_map<TPL>(a);
+    const int lA = mp.lA, tA = mp.tA, lB = mp.lB, tB = mp.tB;
 
     // ---- 2. block butterflies (R-point DFT of every line); the mapping switches
     //         from A to B at the first shared-memory exchange
@@ -313,6 +311,10 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     if (a.ring == 1 && a.discard) {
         __syncthreads();
         constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
+        int64_t io, u0, u1;
+        line_offsets(a, line0 + lA, io, u0, u1);
+        io += ring_off;
+        const V *in = reinterpret_cast<const V *>(a.in);
 #pragma unroll
         for (int m = 0; m < P; m++) {
             const V *p = in + io + int64_t(tA + m * TPL) * a.in_kstr;
@@ -324,6 +326,9 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     // ---- 3. lifted weights w_N^{(e k) mod N} for k = tB + m R/P: one two-level
     //         lookup for k = tB, one for the increment, then a multiplicative chain
     //         in double precision (<= 15 products, ~1e-15 relative)
+    int64_t oo, te, u0;
+    line_offsets(a, line0 + lB, u0, oo, te);
+    if (a.ring == 2) oo += ring_off;
     if (a.twmask) {
         const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
         const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
@@ -350,6 +355,27 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
             for (int m = 0; m < P; m++) st_pol(out + oo + kaddr(a, tB + m * TPL), pts[m], pol);
         }
     }
+}
+
+// One tile with direct (register) loads -- the non-pipelined form.
+template <typename V, int LR>
+__device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
+    constexpr int LP = LR < 4 ? LR : 4;
+    constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
+    const TileMap mp = tile_map<TPL>(a);
+    int64_t io, u0, u1;
+    line_offsets(a, line0 + mp.lA, io, u0, u1);
+    if (a.ring == 1) io += ring_off;
+    V pts[P];
+    // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
+    {
+        const uint64_t pol = l2_policy(a.ring == 1);
+        const V *base = reinterpret_cast<const V *>(a.in) + io + int64_t(mp.tA) * a.in_kstr;
+        const int64_t step = int64_t(TPL) * a.in_kstr;
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = ld_pol(base + m * step, pol);
+    }
+    tile_compute<V, LR>(a, line0, sm, ring_off, pts);
 }
 
 template <typename V, int LR>
@@ -521,12 +547,12 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                      const DevTables &tb, cudaStream_t stream) {
     int64_t nlines = 0;
     KArgs a = fill_args(d, in, out, tb, &nlines);
+    const int64_t tiles = nlines / d.W;
     KFn<V> fn = tab[d.logR];
     if (d.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
         if (e != cudaSuccess) return e;
     }
-    const int64_t tiles = nlines / d.W;
     fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
     return cudaGetLastError();
 }

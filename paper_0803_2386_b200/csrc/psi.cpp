@@ -64,7 +64,10 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int64_t ext0 = d.ndig ? d.ext[0] : 1;
     // Lines per tile: enough adjacent lines for full 128-byte runs on a
     // line-coalesced side; enough threads per CTA otherwise.
-    int64_t W = lf ? slots : (TPL >= 256 ? 1 : 256 / TPL);
+    // (point-contiguous lines of >= 2^10 points: one line per CTA -- more, smaller
+    // CTAs per SM overlap their load and compute phases better; measured cfg5
+    // z-pass 7.48 -> 6.84 ms)
+    int64_t W = lf ? slots : (TPL >= 64 ? 1 : 256 / TPL);
     // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
     // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
     // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
@@ -72,6 +75,9 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int64_t kbytes = (d.in_kstr > d.out_kstr ? d.in_kstr : d.out_kstr) * esize;
     const char *cap_env = std::getenv("MOA_FFT_SMEM_CAP");
     const int64_t smem_cap = cap_env ? std::atoll(cap_env) : (lf && kbytes >= (int64_t(1) << 20) ? 200000 : 100 * 1024);
+    // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
+    const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
+    if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
@@ -506,11 +512,12 @@ static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, con
 
 moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::vector<int64_t> &radices, bool planned,
                        std::vector<moa_pass_desc_t> &out) {
-    const char *fz = std::getenv("MOA_FFT_FUSE");
+    // the four-factor lifting as two L2-staged pairs is opt-in (MOA_FFT_LIFT4=1):
+    // measured round 1, the four plain passes are faster (cfg3 5.55 vs 6.70 ms,
+    // cfg4 12.9 vs 21.5 ms)
+    (void)planned;
     const char *l4 = std::getenv("MOA_FFT_LIFT4");
-    const bool fuse = !(fz && fz[0] == '0');
-    if (fuse && radices.size() == 4 && (planned || (l4 && l4[0] == '1')) && radices[0] == radices[1] &&
-        radices[2] == radices[3]) {
+    if (l4 && l4[0] == '1' && radices.size() == 4 && radices[0] == radices[1] && radices[2] == radices[3]) {
         std::vector<moa_pass_desc_t> v;
         if (lift4_fused(n, batch, dtype, radices.data(), v) == MOA_OK) {
             out.swap(v);
@@ -538,10 +545,11 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
         radices.push_back(n);
         return MOA_OK;
     }
-    // large transforms: four factors (R, R, R', R') run as two L2-staged pairs
-    // -> two HBM round trips (see lift4_fused); needs an even t
-    const char *fz = std::getenv("MOA_FFT_FUSE");
-    if (t >= 24 && t % 2 == 0 && t <= 36 && !(fz && fz[0] == '0')) {
+    // large transforms: four balanced factors (R, R, R', R') of <= 2^8 points,
+    // each pass one shared-memory exchange (the L1/smem data path
+    // costs one 16-byte move per load, store and exchange half, so passes with two
+    // exchanges (R = 2^9, 2^10) run below the HBM roofline); needs an even t
+    if (t >= 26 && t % 2 == 0 && t <= 32) {
         const int a = (t + 3) / 4, b = t / 2 - a;
         for (int x : {a, a, b, b}) radices.push_back(int64_t(1) << x);
         return MOA_OK;

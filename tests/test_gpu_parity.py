@@ -103,7 +103,8 @@ def test_fused_pairs(m, torch_cuda, monkeypatch, fuse, n, batch, dtype, radices)
 
 @pytest.mark.parametrize("n,batch,dtype,radices", [
     (1 << 20, 3, "c128", [32, 32, 32, 32]), (1 << 22, 2, "c64", [64, 64, 32, 32]),
-    (1 << 24, 1, "c128", None), (1 << 24, 1, "c64", None), (1 << 26, 1, "c64", None),
+    (1 << 24, 1, "c128", [64, 64, 64, 64]), (1 << 24, 1, "c64", [64, 64, 64, 64]),
+    (1 << 26, 1, "c64", [128, 128, 64, 64]),
 ])
 def test_lift4_fused_pairs(m, torch_cuda, monkeypatch, n, batch, dtype, radices):
     # large single transforms: four factors as two L2-staged pairs (two HBM round trips)
