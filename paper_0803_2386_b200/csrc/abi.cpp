@@ -113,9 +113,25 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
         if (it != byR.end()) {
             t.twR = it->second;
         } else {
+            // step twiddles of the in-register Stockham schedule of kernels.cu
+            // (steps of radix 16, the last takes the remainder): step s with
+            // NS = 16^s points already combined and radix Q stores
+            // w_{NS Q}^{jm r} (1 <= r < Q, jm < NS) at entry r NS + jm - 1; the
+            // steps tile [0, R - 1) exactly (sum_s (Q_s - 1) NS_s = R - 1)
             const int64_t R = int64_t(1) << d.logR;
-            std::vector<long double> v(2 * R);
-            for (int64_t e = 0; e < R; e++) omega_ld(e, R, v[2 * e], v[2 * e + 1]);
+            const int LP = d.logR < 4 ? d.logR : 4;
+            const int nstep = d.logR == 0 ? 1 : (d.logR + LP - 1) / LP;
+            std::vector<long double> v(2 * (R > 1 ? R - 1 : 1), 0.0L);
+            for (int st = 1; st < nstep; st++) {
+                const int64_t NS = int64_t(1) << (LP * st);
+                const int lq = st == nstep - 1 ? d.logR - LP * (nstep - 1) : LP;
+                const int64_t Q = int64_t(1) << lq;
+                for (int64_t r = 1; r < Q; r++)
+                    for (int64_t jm = 0; jm < NS; jm++) {
+                        const int64_t idx = r * NS + jm - 1;
+                        omega_ld((jm * r) % (NS * Q), NS * Q, v[2 * idx], v[2 * idx + 1]);
+                    }
+            }
             moa_status_t st = upload_table(p, v, &t.twR);
             if (st) return st;
             byR[d.logR] = t.twR;

@@ -202,7 +202,9 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
         if constexpr (NS > 1) {
             const int jm = j & (NS - 1);
 #pragma unroll
-            for (int r = 1; r < Q; r++) v[r] = cmul(v[r], __ldg(twR + ((jm * r) << (LR - LNS - LQ))));
+            // step twiddle w_{NS Q}^{jm r} from the step-major table (entry r NS + jm - 1):
+            // the lanes of a warp read consecutive (or equal) entries
+            for (int r = 1; r < Q; r++) v[r] = cmul(v[r], __ldg(twR + (r * NS + jm - 1)));
         }
         dft_reg<LQ>(v);
         if constexpr (!LAST) {

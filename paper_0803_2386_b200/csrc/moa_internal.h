@@ -36,7 +36,7 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype);
 
 // kernels.cu
 struct DevTables {
-    const void *twR = nullptr;   // w_R^e, e < R (this pass's in-line step twiddles)
+    const void *twR = nullptr;   // this pass's in-line Stockham step twiddles (step-major, R - 1 entries)
     const void *tw_hi = nullptr; // w_N^{eh 2^h}
     const void *tw_lo = nullptr; // w_N^{el}
 };
