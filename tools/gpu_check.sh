@@ -18,3 +18,11 @@ if [ "${NCU:-1}" = 1 ]; then
       --log-file gpurun_out/launches_$W.csv $CMD > gpurun_out/ncu_$W.log 2>&1
   echo "ncu exit $?" >> gpurun_out/bench_status.txt
 fi
+if [ "${NCU_FULL:-0}" = 1 ]; then
+  W=${NCU_WORKLOAD:-cfg2}
+  CMD="python bench.py --workload $W --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+  $CMD > gpurun_out/ncu_plain_full_$W.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_REGEX:-pass_kernel}" \
+      -s ${NCU_SKIP:-6} -c ${NCU_COUNT:-2} -o gpurun_out/full_$W $CMD > gpurun_out/ncu_full_$W.log 2>&1
+  echo "ncu full exit $?" >> gpurun_out/bench_status.txt
+fi
