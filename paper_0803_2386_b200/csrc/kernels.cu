@@ -404,9 +404,9 @@ struct PairArgs {
     unsigned long long *stats;  // optional wait statistics (6 counters), or null
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -445,36 +445,61 @@ __global__ void __launch_bounds__(512) pair_kernel(const __grid_constant__ PairA
     // the per-group completion counters only ever grow, by exactly TA / TB per launch
     const unsigned long long round = p.epoch + 1;
     V *sm = reinterpret_cast<V *>(smem_raw);
+    // Deadlock freedom: every CTA is resident and every wait is on a smaller
+    // position; the smallest unfinished position is some CTA's current (or
+    // fetched-ahead) tile, whose dependencies are all finished and published
+    // (a CTA publishes its previous tile before it ever spins).
+    bool have_prev = false, prev_B = false;
+    int64_t prev_g = 0;
     // Static round-robin over the tile order (tile pos -> CTA pos mod grid, each
-    // CTA in increasing order).  With every CTA resident, the smallest unfinished
-    // tile is always some CTA's current tile and all it waits on is smaller, so
-    // the schedule cannot deadlock -- and no queue atomic is needed.
+    // CTA in increasing order; an atomic queue measured slower).
     for (int64_t pos = blockIdx.x; pos < total; pos += gridDim.x) {
         bool isB;
         int64_t g, idx;
         decode_tile(p, pos, isB, g, idx);
+        bool signalled = false;  // (thread 0) the previous tile's completion already published
         if (threadIdx.x == 0) {
-            // (a watchdog turns a broken schedule into a launch error instead of a hang)
-            unsigned spins = 0;
-            const long long t0 = p.stats ? clock64() : 0;
+            // relaxed polling (no L1 invalidation per poll: every ring access is
+            // an L2 (.cg) access); a watchdog turns a broken schedule into a
+            // launch error instead of a hang.  A CTA never spins while holding
+            // an unpublished completion (that could close a wait cycle), so the
+            // previous tile is published first whenever a wait is needed.
+            const unsigned long long *dep = nullptr;
+            unsigned long long need = 0;
             if (isB) {
-                while (ld_acquire(p.cntA + g) < round * (unsigned long long)p.TA) {
-                    __nanosleep(64);
-                    if (++spins > (1u << 26)) __trap();
-                }
+                dep = p.cntA + g;
+                need = round * (unsigned long long)p.TA;
             } else if (g > p.slot_mask) {
-                while (ld_acquire(p.cntB + g - (p.slot_mask + 1)) < round * (unsigned long long)p.TB) {
-                    __nanosleep(64);
+                dep = p.cntB + g - (p.slot_mask + 1);
+                need = round * (unsigned long long)p.TB;
+            }
+            if (dep && ld_relaxed(dep) < need) {
+                if (have_prev) {
+                    __threadfence();
+                    atomicAdd(prev_B ? p.cntB + prev_g : p.cntA + prev_g, 1ull);
+                    signalled = true;
+                }
+                unsigned spins = 0;
+                const long long t0 = p.stats ? clock64() : 0;
+                while (ld_relaxed(dep) < need) {
+                    __nanosleep(32);
                     if (++spins > (1u << 26)) __trap();
                 }
-            }
-            if (p.stats && spins) {  // MOA_FFT_STATS: waits, spins, wait cycles
-                atomicAdd(p.stats + (isB ? 0 : 3), 1ull);
-                atomicAdd(p.stats + (isB ? 1 : 4), (unsigned long long)spins);
-                atomicAdd(p.stats + (isB ? 2 : 5), (unsigned long long)(clock64() - t0));
+                if (p.stats) {  // MOA_FFT_STATS: waits, spins, wait cycles
+                    atomicAdd(p.stats + (isB ? 0 : 3), 1ull);
+                    atomicAdd(p.stats + (isB ? 1 : 4), (unsigned long long)spins);
+                    atomicAdd(p.stats + (isB ? 2 : 5), (unsigned long long)(clock64() - t0));
+                }
             }
         }
         __syncthreads();
+        // otherwise the previous tile (all its stores were issued before the two
+        // barriers since) is published here, so the fence's latency overlaps
+        // this tile's loads in the other warps instead of stalling the CTA
+        if (threadIdx.x == 0 && have_prev && !signalled) {
+            __threadfence();
+            atomicAdd(prev_B ? p.cntB + prev_g : p.cntA + prev_g, 1ull);
+        }
         const int64_t ring_off = (g & p.slot_mask) * p.ringG;
         if constexpr (LRA == LRB) {
             // one inlined tile body for both passes (the fused kernel otherwise
@@ -487,10 +512,13 @@ __global__ void __launch_bounds__(512) pair_kernel(const __grid_constant__ PairA
             else tile_body<V, LRA>(p.A, (g * p.TA + idx) * p.A.W, sm, ring_off);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(isB ? p.cntB + g : p.cntA + g, 1ull);
-        }
+        have_prev = true;
+        prev_B = isB;
+        prev_g = g;
+    }
+    if (threadIdx.x == 0 && have_prev) {
+        __threadfence();
+        atomicAdd(prev_B ? p.cntB + prev_g : p.cntA + prev_g, 1ull);
     }
 }
 

@@ -431,9 +431,11 @@ static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, con
         if (R[i] < 32 || R[i] > 1024) return fail(MOA_EUNSUPPORTED, "psi: lift4 radices must be in [32, 1024]");
     const int64_t G01 = R0 * R1 * W, G23 = W * R2 * R3;
     const int64_t g01 = (S1 / W) * batch, g23 = R1 * (R0 / W) * batch;
+    const char *mb = std::getenv("MOA_FFT_RING_MB");  // ablation: ring size budget
+    const int64_t budget = mb ? std::atoll(mb) << 20 : int64_t(32) << 20;
     auto ring = [&](moa_pass_desc_t &d, int side, int64_t groups, int64_t G) {
         int64_t slots = 4;
-        while (slots * 2 * G * esize <= (int64_t(32) << 20) && slots < 64 && slots * 2 <= groups) slots *= 2;
+        while (slots * 2 * G * esize <= budget && slots < 256 && slots * 2 <= groups) slots *= 2;
         d.ring = side;
         d.ring_slots = int32_t(slots);
         d.ring_lag = int32_t(slots / 2);

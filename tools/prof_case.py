@@ -44,3 +44,4 @@ for i in range(a.reps):
 per, nex = m.moa_fft_prof_end(plan.h)
 print("per-launch ms:", [round(v / max(nex, 1), 3) for v in per])
 print([(d["logR"], d["W"], d["threads"], d["smem_bytes"]) for d in plan.describe()])
+plan.close()  # prints MOA_FFT_STATS ring statistics, if enabled
