@@ -47,7 +47,10 @@ def _load():
             "orc_bitrev": [vp, i64],
             "orc_fft_radix2": [vp, i64],
             "orc_fft_radix2_batch": [vp, i64, i64],
+            "orc_fft_radix2_sign": [vp, i64, ctypes.c_int],
+            "orc_fft_radix2_batch_sign": [vp, i64, i64, ctypes.c_int],
             "orc_dft_direct": [vp, vp, i64],
+            "orc_dft_direct_sign": [vp, vp, i64, ctypes.c_int],
             "orc_dft_bins": [vp, vp, i64, vp, vp, i64, vp],
             "orc_dft3_bins": [vp, i64, i64, i64, vp, i64, vp],
             "orc_reshape_transpose": [vp, vp, i64, i64],
@@ -55,6 +58,7 @@ def _load():
             "orc_lifted_plan": [i64, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
             "orc_fft_lifted": [vp, i64, i64],
             "orc_fft3d": [vp, i64, i64, i64],
+            "orc_fft3d_sign": [vp, i64, i64, i64, ctypes.c_int],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -95,6 +99,29 @@ def fft_radix2(x) -> np.ndarray:
     a = _c128(x).copy()
     _check(_load().orc_fft_radix2(a.ctypes.data, a.size), "fft_radix2")
     return a
+
+
+def fft_radix2_sign(x, sign: int) -> np.ndarray:
+    """O1+O2 with kernel e^{sign 2 pi i jk/n}: sign=-1 forward; sign=+1 the
+    fragment's EXP(+2 pi i row/L), the unnormalised inverse."""
+    a = _c128(x).copy()
+    _check(_load().orc_fft_radix2_sign(a.ctypes.data, a.size, sign), "fft_radix2_sign")
+    return a
+
+
+def fft_radix2_rows_sign(x, n: int, sign: int) -> np.ndarray:
+    a = _c128(x).copy()
+    assert a.size % n == 0
+    _check(_load().orc_fft_radix2_batch_sign(a.ctypes.data, n, a.size // n, sign), "fft_radix2_batch_sign")
+    return a
+
+
+def dft_direct_sign(x, sign: int) -> np.ndarray:
+    """O3 with kernel e^{sign 2 pi i jk/n}."""
+    a = _c128(x)
+    out = np.empty_like(a)
+    _check(_load().orc_dft_direct_sign(a.ctypes.data, out.ctypes.data, a.size, sign), "dft_direct_sign")
+    return out
 
 
 def fft_radix2_inplace(a: np.ndarray) -> np.ndarray:
@@ -182,6 +209,14 @@ def fft3d(x) -> np.ndarray:
     a = np.ascontiguousarray(np.asarray(x), dtype=np.complex128).copy()
     assert a.ndim == 3
     _check(_load().orc_fft3d(a.ctypes.data, *a.shape), "fft3d")
+    return a
+
+
+def fft3d_sign(x, sign: int) -> np.ndarray:
+    """O5 with kernel e^{sign 2 pi i (...)} (sign=+1: the unnormalised inverse)."""
+    a = np.ascontiguousarray(np.asarray(x), dtype=np.complex128).copy()
+    assert a.ndim == 3
+    _check(_load().orc_fft3d_sign(a.ctypes.data, *a.shape, sign), "fft3d_sign")
     return a
 
 

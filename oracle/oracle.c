@@ -143,11 +143,15 @@ static void radix2_stage(double *x, int64_t n, int64_t L, const double *wt) {
     }
 }
 
-/* Forward, unnormalised DFT of x (length n = 2^t, t >= 0) in place:
- * x <- P_n x (Fig. vanloan_fft line 1), then the q = 1..t stages of
- * Fig. fftpsirad2.  Returns -1 if n is not a power of two. */
-int orc_fft_radix2(double *x, int64_t n) {
+/* Unnormalised DFT of x (length n = 2^t, t >= 0) in place with kernel
+ * e^{sign 2 pi i jk/n}: x <- P_n x (Fig. vanloan_fft line 1), then the
+ * q = 1..t stages of Fig. fftpsirad2.  sign = -1 is the forward transform
+ * (reading R1); sign = +1 is the fragment's own weight EXP(+2 pi i row/L)
+ * read literally, the unnormalised inverse.  Returns -1 if n is not a
+ * power of two or sign is not +-1. */
+int orc_fft_radix2_sign(double *x, int64_t n, int sign) {
     int t = ilog2_exact(n);
+    if (sign != 1 && sign != -1) return -1;
     if (t < 0) return -1;
     if (n == 1) return 0;
     orc_bitrev(x, n);
@@ -158,9 +162,9 @@ int orc_fft_radix2(double *x, int64_t n) {
 #pragma omp parallel for schedule(static) if (L >= 65536)
         for (int64_t row = 0; row < L / 2; row++) {
             long double re, im;
-            omega(row, L, &re, &im);
+            omega(row, L, &re, &im); /* e^{-2 pi i row/L} */
             wt[2 * row] = (double)re;
-            wt[2 * row + 1] = (double)im;
+            wt[2 * row + 1] = sign < 0 ? (double)im : -(double)im;
         }
         radix2_stage(x, n, L, wt);
     }
@@ -168,22 +172,27 @@ int orc_fft_radix2(double *x, int64_t n) {
     return 0;
 }
 
+/* The forward transform (the BASELINE.json semantics). */
+int orc_fft_radix2(double *x, int64_t n) { return orc_fft_radix2_sign(x, n, -1); }
+
 /* Independent rows (cfg2 "batch contiguous rows"): row b is x[b*n .. b*n+n). */
-int orc_fft_radix2_batch(double *x, int64_t n, int64_t batch) {
+int orc_fft_radix2_batch_sign(double *x, int64_t n, int64_t batch, int sign) {
     if (ilog2_exact(n) < 0 || batch < 0) return -1;
     for (int64_t b = 0; b < batch; b++) {
-        int rc = orc_fft_radix2(x + 2 * b * n, n);
+        int rc = orc_fft_radix2_sign(x + 2 * b * n, n, sign);
         if (rc) return rc;
     }
     return 0;
 }
 
+int orc_fft_radix2_batch(double *x, int64_t n, int64_t batch) { return orc_fft_radix2_batch_sign(x, n, batch, -1); }
+
 /* ---- O3: the definition ---------------------------------------------------- */
 /* X[k] = sum_j x[j] T[(j k) mod n], T[e] = e^{-2 pi i e/n}; the exponent is
  * reduced in integers before forming the angle; long double accumulation.
  * Any n >= 1 (the definition does not need a power of two). */
-int orc_dft_direct(const double *x, double *X, int64_t n) {
-    if (n < 1) return -1;
+int orc_dft_direct_sign(const double *x, double *X, int64_t n, int sign) {
+    if (n < 1 || (sign != 1 && sign != -1)) return -1;
     long double *T = (long double *)malloc(sizeof(long double) * 2 * (size_t)n);
     if (!T) return -2;
     for (int64_t e = 0; e < n; e++) omega(e, n, &T[2 * e], &T[2 * e + 1]);
@@ -192,7 +201,7 @@ int orc_dft_direct(const double *x, double *X, int64_t n) {
         long double sr = 0.0L, si = 0.0L;
         for (int64_t j = 0; j < n; j++) {
             int64_t e = (int64_t)(((unsigned __int128)j * (unsigned __int128)k) % (unsigned __int128)n);
-            long double tr = T[2 * e], ti = T[2 * e + 1];
+            long double tr = T[2 * e], ti = sign < 0 ? T[2 * e + 1] : -T[2 * e + 1];
             long double xr = x[2 * j], xi = x[2 * j + 1];
             sr += xr * tr - xi * ti;
             si += xr * ti + xi * tr;
@@ -203,6 +212,9 @@ int orc_dft_direct(const double *x, double *X, int64_t n) {
     free(T);
     return 0;
 }
+
+/* X[k] = sum_j x[j] e^{-2 pi i jk/n}: the forward definition. */
+int orc_dft_direct(const double *x, double *X, int64_t n) { return orc_dft_direct_sign(x, X, n, -1); }
 
 /* w_n^e for 0 <= e < n via e = eh*2^h + el: w^e = w^{eh 2^h} * w^{el}.  Both
  * factors are exact-exponent direct evaluations (long double); this is only a
@@ -415,8 +427,9 @@ int orc_fft_lifted(double *x, int64_t n, int64_t c) {
 /* ---- O5: 3-D ------------------------------------------------------------------ */
 /* Row-major [n0][n1][n2]; 1-D FFTs along axis 2 (contiguous lines), then axis 1,
  * then axis 0.  Each line is gathered, transformed by orc_fft_radix2, scattered. */
-int orc_fft3d(double *x, int64_t n0, int64_t n1, int64_t n2) {
+int orc_fft3d_sign(double *x, int64_t n0, int64_t n1, int64_t n2, int sign) {
     if (ilog2_exact(n0) < 0 || ilog2_exact(n1) < 0 || ilog2_exact(n2) < 0) return -1;
+    if (sign != 1 && sign != -1) return -1;
     int64_t dims[3] = {n0, n1, n2};
     int64_t strides[3] = {n1 * n2, n2, 1};
     for (int ax = 2; ax >= 0; ax--) {
@@ -439,7 +452,7 @@ int orc_fft3d(double *x, int64_t n0, int64_t n1, int64_t n2) {
                     line[2 * j] = x[2 * (base + j * st)];
                     line[2 * j + 1] = x[2 * (base + j * st) + 1];
                 }
-                orc_fft_radix2(line, len);
+                orc_fft_radix2_sign(line, len, sign);
                 for (int64_t j = 0; j < len; j++) {
                     x[2 * (base + j * st)] = line[2 * j];
                     x[2 * (base + j * st) + 1] = line[2 * j + 1];
@@ -451,3 +464,5 @@ int orc_fft3d(double *x, int64_t n0, int64_t n1, int64_t n2) {
     }
     return 0;
 }
+
+int orc_fft3d(double *x, int64_t n0, int64_t n1, int64_t n2) { return orc_fft3d_sign(x, n0, n1, n2, -1); }

@@ -239,3 +239,40 @@ def test_fft3d_plane_wave():
     assert abs(y[k] - N) < 1e-9
     y[k] = 0
     assert np.max(np.abs(y)) < 1e-9
+
+
+# ---------------------------------------------------------------- the + sign (inverse) variant
+@pytest.mark.parametrize("t", [0, 1, 5, 10])
+def test_plus_sign_direct_vs_textbook_and_radix2(t):
+    # the fragment's weight EXP(+2 pi i row/L) read literally: kernel e^{+2 pi i jk/n}
+    n = 1 << t
+    x = rand(n, 300 + t)
+    j = np.arange(n)
+    F = np.exp(2j * np.pi * (np.outer(j, j) % n) / n)                   # the written-out matrix
+    assert rel_l2(oracle.dft_direct_sign(x, +1), F @ x) < 1e-13
+    assert rel_l2(oracle.fft_radix2_sign(x, +1), oracle.dft_direct_sign(x, +1)) < 1e-14
+    assert rel_l2(oracle.fft_radix2_sign(x, -1), oracle.fft_radix2(x)) == 0.0
+
+
+@pytest.mark.parametrize("t", [1, 8, 16])
+def test_plus_sign_closed_forms_and_roundtrip(t):
+    n = 1 << t
+    eps = 10 * n * np.finfo(float).eps
+    # impulse at k0 -> e^{+2 pi i k0 j / n} (the inverse of the forward closed form)
+    k0 = (5 * n) // 11
+    d = np.zeros(n, np.complex128)
+    d[k0] = 1
+    j = np.arange(n)
+    assert np.max(np.abs(oracle.fft_radix2_sign(d, +1) - np.exp(2j * np.pi * ((k0 * j) % n) / n))) < eps
+    # forward then + sign returns n x (the unnormalised inverse), numpy.fft.ifft as third party
+    x = rand(n, 400 + t)
+    assert rel_l2(oracle.fft_radix2_sign(oracle.fft_radix2(x), +1), n * x) < 1e-14
+    assert rel_l2(oracle.fft_radix2_sign(x, +1), n * np.fft.ifft(x)) < 1e-13
+    rows = oracle.fft_radix2_rows_sign(np.concatenate([x, 2 * x]), n, +1)
+    assert rel_l2(rows[n:], 2 * rows[:n]) < 1e-15
+
+
+def test_plus_sign_3d():
+    x = rand(4 * 8 * 16, 77).reshape(4, 8, 16)
+    assert rel_l2(oracle.fft3d_sign(x, +1), 512 * np.fft.ifftn(x)) < 1e-13
+    assert rel_l2(oracle.fft3d_sign(oracle.fft3d(x), +1), 512 * x) < 1e-14
