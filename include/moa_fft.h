@@ -88,6 +88,42 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
                              int ngpu);
 
 /*
+ * Plan flags (the paper's variants):
+ *   MOA_FFT_INVERSE      kernel e^{+2 pi i jk/n} -- the sign of the fftpsirad2
+ *                        fragment's weight EXP(+2 pi i row/L) (reading R1).
+ *   MOA_FFT_NORMALIZE    multiply the result by 1/N (N = n, or n0 n1 n2; exact,
+ *                        N is a power of two).  With INVERSE this is the inverse DFT.
+ *   MOA_FFT_LIFTED_ORDER 1-D only: leave X in the lifting's own order instead of
+ *                        applying the final transpose -- the paper's "far more
+ *                        efficient approach in which no data needs to be moved"
+ *                        (P:2983-2984).  Where X[k] lands is given by
+ *                        moa_fft_output_index().  On one GPU the last pass then
+ *                        stores in place (its own load positions); with ngpu > 1
+ *                        the third all-to-all and the unpack are skipped and rank g
+ *                        holds X[g + p k2] at offset k2 (the rank is the fastest
+ *                        output digit).  A plan may keep natural order (identity
+ *                        map) where that costs nothing extra (single-pass plans).
+ * Unknown bits -> MOA_EINVAL; LIFTED_ORDER on a 3-D plan -> MOA_EUNSUPPORTED.
+ */
+#define MOA_FFT_INVERSE 1u
+#define MOA_FFT_NORMALIZE 2u
+#define MOA_FFT_LIFTED_ORDER 4u
+
+/* moa_fft_plan / moa_fft_plan_3d with flags (0 = the forward, natural-order plan). */
+moa_status_t moa_fft_plan_ex(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,
+                             uint32_t flags);
+moa_status_t moa_fft_plan_3d_ex(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
+                                int ngpu, uint32_t flags);
+
+/*
+ * moa_fft_output_index -- where a 1-D plan stores each output: pos[k] (k < n)
+ * is the element offset of X[k] within the row (ngpu = 1; row b adds b*n), or
+ * the global offset g*(n/p) + local offset (ngpu > 1: rank g's out block).
+ * Natural order gives pos[k] = k.  `count` must equal n.  Host only.
+ */
+moa_status_t moa_fft_output_index(moa_fft_plan_t plan, int64_t *pos, int64_t count);
+
+/*
  * moa_fft_exec -- run the plan on device buffers, stream-ordered on `stream`
  * (a cudaStream_t of the plan's device; NULL = legacy default stream).
  *   in  : device pointer, `local elements` complex values (n*batch at ngpu=1),
@@ -159,11 +195,13 @@ moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, const void *
  * i < nsteps are kinds[i] = 0 (run passes[srcs[i]]) or 1 (all-to-all of
  * counts[i] complex elements per peer from buffer srcs[i] to dsts[i]; buffer
  * ids 0 in, 1 out, 2 scratch, 3 scratch2).  is3d = 0: n0 is the 1-D length.
+ * flags: MOA_FFT_LIFTED_ORDER selects the 1-D schedule without the third
+ * all-to-all and the unpack (other bits do not change the schedule).
  */
 moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
                                void *passes /* moa_pass_desc_t[max_passes] */, int max_passes, int *npasses,
                                int32_t *kinds, int32_t *srcs, int32_t *dsts, int64_t *counts, int max_steps,
-                               int *nsteps);
+                               int *nsteps, uint32_t flags);
 
 /*
  * psi-index layer introspection (host only, no GPU needed).

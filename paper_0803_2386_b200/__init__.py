@@ -15,6 +15,7 @@ _SO = os.path.join(_HERE, "libmoafft.so")
 
 MOA_OK, MOA_EINVAL, MOA_ENOMEM, MOA_ECUDA, MOA_ENCCL, MOA_EUNSUPPORTED = range(6)
 MOA_C64, MOA_C128 = 0, 1
+MOA_FFT_INVERSE, MOA_FFT_NORMALIZE, MOA_FFT_LIFTED_ORDER = 1, 2, 4
 MAX_DIGITS = 6
 MAX_PASSES = 16
 STATUS_NAMES = {0: "MOA_OK", 1: "MOA_EINVAL", 2: "MOA_ENOMEM", 3: "MOA_ECUDA", 4: "MOA_ENCCL",
@@ -27,6 +28,7 @@ EXPORTS = [
     "moa_fft_get_unique_id", "moa_fft_dist_init", "moa_fft_dist_finalize", "moa_fft_dist_loopback",
     "moa_fft_exec_loopback", "moa_dist_describe", "moa_psi_describe", "moa_psi_describe_3d",
     "moa_plan_radices", "moa_fft_plan_describe", "moa_fft_prof_begin", "moa_fft_prof_end",
+    "moa_fft_plan_ex", "moa_fft_plan_3d_ex", "moa_fft_output_index",
 ]
 
 
@@ -77,6 +79,9 @@ def _load():
         "moa_fft_plan": [P(vp), i64, i64, i32, i32],
         "moa_fft_plan_lift": [P(vp), i64, i64, i32, P(i64), i32],
         "moa_fft_plan_3d": [P(vp), i64, i64, i64, i32, i32],
+        "moa_fft_plan_ex": [P(vp), i64, i64, i32, i32, ctypes.c_uint32],
+        "moa_fft_plan_3d_ex": [P(vp), i64, i64, i64, i32, i32, ctypes.c_uint32],
+        "moa_fft_output_index": [vp, P(i64), i64],
         "moa_fft_exec": [vp, vp, vp, vp],
         "moa_fft_exec_host": [vp, vp, vp, vp],
         "moa_fft_destroy": [vp],
@@ -86,7 +91,7 @@ def _load():
         "moa_fft_dist_loopback": [i32, i32],
         "moa_fft_exec_loopback": [P(vp), i32, P(vp), P(vp), vp],
         "moa_dist_describe": [i32, i32, i32, i64, i64, i64, i32, vp, i32, P(i32), P(ctypes.c_int32),
-                              P(ctypes.c_int32), P(ctypes.c_int32), P(i64), i32, P(i32)],
+                              P(ctypes.c_int32), P(ctypes.c_int32), P(i64), i32, P(i32), ctypes.c_uint32],
         "moa_psi_describe": [i64, i64, i32, P(i64), i32, P(PassDesc), i32, P(i32)],
         "moa_psi_describe_3d": [i64, i64, i64, i32, P(PassDesc), i32, P(i32)],
         "moa_plan_radices": [i64, i64, i32, P(i64), i32, P(i32)],
@@ -131,6 +136,26 @@ def moa_fft_plan(n: int, batch: int = 1, dtype="c128", ngpu: int = 1) -> int:
     h = ctypes.c_void_p()
     _check(lib.moa_fft_plan(ctypes.byref(h), n, batch, _dt(dtype), ngpu))
     return h.value
+
+
+def moa_fft_plan_ex(n: int, batch: int = 1, dtype="c128", ngpu: int = 1, flags: int = 0) -> int:
+    h = ctypes.c_void_p()
+    _check(lib.moa_fft_plan_ex(ctypes.byref(h), n, batch, _dt(dtype), ngpu, flags))
+    return h.value
+
+
+def moa_fft_plan_3d_ex(n0: int, n1: int, n2: int, dtype="c128", ngpu: int = 1, flags: int = 0) -> int:
+    h = ctypes.c_void_p()
+    _check(lib.moa_fft_plan_3d_ex(ctypes.byref(h), n0, n1, n2, _dt(dtype), ngpu, flags))
+    return h.value
+
+
+def moa_fft_output_index(plan: int, n: int):
+    """pos[k] = offset where X[k] is stored (see include/moa_fft.h)."""
+    import numpy as np
+    pos = np.empty(n, dtype=np.int64)
+    _check(lib.moa_fft_output_index(plan, pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n))
+    return pos
 
 
 def moa_fft_plan_lift(n: int, batch: int, dtype, radices) -> int:
@@ -237,7 +262,7 @@ def moa_fft_prof_end(plan: int):
     return list(arr[: ns.value]), nx.value
 
 
-def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128") -> dict:
+def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128", flags: int = 0) -> dict:
     """Schedule of one rank: n = N (1-D) or (n0, n1, n2) (3-D slab)."""
     is3d = isinstance(n, (tuple, list))
     n0, n1, n2 = (n if is3d else (n, 0, 0))
@@ -246,7 +271,8 @@ def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128") -> dict:
     kinds, srcs, dsts = (ctypes.c_int32 * 32)(), (ctypes.c_int32 * 32)(), (ctypes.c_int32 * 32)()
     counts = (ctypes.c_int64 * 32)()
     _check(lib.moa_dist_describe(rank, ngpu, int(is3d), n0, n1, n2, _dt(dtype), ctypes.cast(passes, ctypes.c_void_p),
-                                 MAX_PASSES, ctypes.byref(np_), kinds, srcs, dsts, counts, 32, ctypes.byref(ns)))
+                                 MAX_PASSES, ctypes.byref(np_), kinds, srcs, dsts, counts, 32, ctypes.byref(ns),
+                                 flags))
     steps = []
     for i in range(ns.value):
         if kinds[i] == 0:
@@ -261,18 +287,29 @@ class FFTPlan:
     """RAII wrapper: FFTPlan(n, batch, dtype) or FFTPlan.plan_3d(...); exec on
     torch device tensors (complex64 / complex128, contiguous)."""
 
-    def __init__(self, n: int = 0, batch: int = 1, dtype="c128", ngpu: int = 1, radices=None, _handle=None):
+    def __init__(self, n: int = 0, batch: int = 1, dtype="c128", ngpu: int = 1, radices=None, _handle=None,
+                 inverse: bool = False, normalize: bool = False, lifted_order: bool = False):
+        flags = (MOA_FFT_INVERSE if inverse else 0) | (MOA_FFT_NORMALIZE if normalize else 0) | \
+            (MOA_FFT_LIFTED_ORDER if lifted_order else 0)
         if _handle is not None:
             self.h = _handle
         elif radices is not None:
+            if flags:
+                raise ValueError("explicit radices take no flags")
             self.h = moa_fft_plan_lift(n, batch, dtype, radices)
         else:
-            self.h = moa_fft_plan(n, batch, dtype, ngpu)
+            self.h = moa_fft_plan_ex(n, batch, dtype, ngpu, flags)
         self.dtype = _dt(dtype)
+        self.n = n
 
     @classmethod
-    def plan_3d(cls, n0, n1, n2, dtype="c128", ngpu: int = 1):
-        return cls(_handle=moa_fft_plan_3d(n0, n1, n2, dtype, ngpu), dtype=dtype)
+    def plan_3d(cls, n0, n1, n2, dtype="c128", ngpu: int = 1, inverse: bool = False, normalize: bool = False):
+        flags = (MOA_FFT_INVERSE if inverse else 0) | (MOA_FFT_NORMALIZE if normalize else 0)
+        return cls(_handle=moa_fft_plan_3d_ex(n0, n1, n2, dtype, ngpu, flags), dtype=dtype)
+
+    def output_index(self):
+        """pos[k]: where X[k] is stored (identity for natural order)."""
+        return moa_fft_output_index(self.h, self.n)
 
     @property
     def local_elems(self) -> int:

@@ -28,6 +28,15 @@ static moa_status_t cuda_fail(cudaError_t e, const char *what) {
     return fail(MOA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+PassMods pass_mods(uint32_t flags, size_t i, size_t npass, int64_t N) {
+    PassMods m;
+    const bool inv = flags & MOA_FFT_INVERSE;
+    m.conj_in = inv && i == 0;
+    m.conj_out = inv && i + 1 == npass;
+    if ((flags & MOA_FFT_NORMALIZE) && i + 1 == npass) m.scale = 1.0 / double(N);
+    return m;
+}
+
 }  // namespace moa
 
 using namespace moa;
@@ -41,6 +50,9 @@ struct moa_fft_plan_s {
     int64_t n = 0, batch = 1, n0 = 0, n1 = 0, n2 = 0;
     int64_t local_elems = 0;
     size_t esize = 16;
+    uint32_t flags = 0;              // MOA_FFT_INVERSE / _NORMALIZE / _LIFTED_ORDER
+    bool lifted_out = false;         // one GPU: the last pass stores in place (no final transpose)
+    moa_pass_desc_t natural_last{};  // ... and this is the natural-order descriptor it replaced
     std::vector<moa_pass_desc_t> passes;
     std::vector<DevTables> tabs;
     std::vector<void *> allocs;
@@ -223,10 +235,29 @@ moa_status_t finish_plan(moa_fft_plan_s *p) {
     return build_tables(p);
 }
 
+constexpr uint32_t kAllFlags = MOA_FFT_INVERSE | MOA_FFT_NORMALIZE | MOA_FFT_LIFTED_ORDER;
+
+// MOA_FFT_LIFTED_ORDER on one GPU: the last pass stores each result where it
+// loaded its input (point-contiguous, in place) instead of through the final
+// transpose; the natural descriptor is kept for moa_fft_output_index.
+void make_lifted_order(moa_fft_plan_s *p) {
+    if (p->passes.size() < 2) return;  // a single pass is already in natural order
+    moa_pass_desc_t &d = p->passes.back();
+    if (d.ring) return;                // fused L2 pairs keep natural order
+    p->natural_last = d;
+    for (int i = 0; i < d.ndig; i++) d.out_str[i] = d.in_str[i];
+    d.out_kstr = d.in_kstr;
+    d.out_ksplit = 62;
+    d.lf_store = d.lf_load;
+    psi_choose_tile(d, p->dtype);
+    p->lifted_out = true;
+}
+
 moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,
-                     const int64_t *radices, int nrad) {
+                     const int64_t *radices, int nrad, uint32_t flags = 0) {
     if (!plan) return fail(MOA_EINVAL, "plan: null output pointer");
     *plan = nullptr;
+    if (flags & ~kAllFlags) return fail(MOA_EINVAL, "plan: unknown flag bits");
     if (!pow2(n)) return fail(MOA_EINVAL, "plan: n must be a power of two >= 1 (n = 2^t, t >= 0)");
     if (batch < 1) return fail(MOA_EINVAL, "plan: batch must be >= 1");
     if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan: unknown dtype");
@@ -245,9 +276,10 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
     p->ngpu = ngpu;
     p->esize = dtype == MOA_C128 ? 16 : 8;
     p->local_elems = n * batch / ngpu;
+    p->flags = flags;
     moa_status_t st = MOA_OK;
     if (ngpu > 1) {
-        st = dist_plan_1d(p->dist, n, dtype);
+        st = dist_plan_1d(p->dist, n, dtype, (flags & MOA_FFT_LIFTED_ORDER) != 0);
         if (!st) {
             p->passes = p->dist->passes;
             p->rank = p->dist->rank;
@@ -262,6 +294,7 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
             if (!st && !have) st = plan_radices(n, batch, dtype, rad);
         }
         if (!st) st = psi_build(n, batch, dtype, rad, radices == nullptr, p->passes);
+        if (!st && (flags & MOA_FFT_LIFTED_ORDER)) make_lifted_order(p);
     }
     if (!st) st = finish_plan(p);
     if (st) {
@@ -289,9 +322,21 @@ moa_status_t moa_fft_plan_lift(moa_fft_plan_t *plan, int64_t n, int64_t batch, m
     return plan_1d(plan, n, batch, dtype, 1, radices, nrad);
 }
 
+moa_status_t moa_fft_plan_ex(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,
+                             uint32_t flags) {
+    return plan_1d(plan, n, batch, dtype, ngpu, nullptr, 0, flags);
+}
+
 moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype, int ngpu) {
+    return moa_fft_plan_3d_ex(plan, n0, n1, n2, dtype, ngpu, 0);
+}
+
+moa_status_t moa_fft_plan_3d_ex(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype, int ngpu,
+                                uint32_t flags) {
     if (!plan) return fail(MOA_EINVAL, "plan_3d: null output pointer");
     *plan = nullptr;
+    if (flags & ~kAllFlags) return fail(MOA_EINVAL, "plan_3d: unknown flag bits");
+    if (flags & MOA_FFT_LIFTED_ORDER) return fail(MOA_EUNSUPPORTED, "plan_3d: MOA_FFT_LIFTED_ORDER is 1-D only");
     for (int64_t v : {n0, n1, n2})
         if (!pow2(v) || v > 4096) return fail(MOA_EINVAL, "plan_3d: each extent must be a power of two in [1, 4096]");
     if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan_3d: unknown dtype");
@@ -311,6 +356,7 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
     p->ngpu = ngpu;
     p->esize = dtype == MOA_C128 ? 16 : 8;
     p->local_elems = p->n / ngpu;
+    p->flags = flags;
     moa_status_t st;
     if (ngpu > 1) {
         st = dist_plan_3d(p->dist, n0, n1, n2, dtype);
@@ -345,11 +391,12 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     cudaEvent_t *evs = nullptr;
     if (p->prof_count < p->prof_max) evs = &p->prof_ev[size_t(p->prof_count) * (p->prof_nsteps + 1)];
     moa_status_t st = MOA_OK;
+    const size_t np = p->passes.size();
     if (p->dist) {
-        st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs);
+        st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs, p->flags, p->n);
     } else {
         int step = 0;
-        for (size_t i = 0; i < p->passes.size(); i++, step++) {
+        for (size_t i = 0; i < np; i++, step++) {
             const moa_pass_desc_t &d = p->passes[i];
             const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
             if (evs) cudaEventRecord(evs[step], s);
@@ -357,13 +404,14 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
                 const moa_pass_desc_t &dB = p->passes[i + 1];
                 void *dst = dB.dst == 1 ? out : p->scratch;
                 RingState &r = p->rings[i];
-                e = launch_pair(d, dB, p->dtype, src, dst, r, p->tabs[i], p->tabs[i + 1], s);
+                e = launch_pair(d, dB, p->dtype, src, dst, r, p->tabs[i], p->tabs[i + 1], s,
+                                pass_mods(p->flags, i, np, p->n), pass_mods(p->flags, i + 1, np, p->n));
                 if (e != cudaSuccess) return cuda_fail(e, "pass-pair kernel launch");
                 r.epoch++;
                 i++;
             } else {
                 void *dst = d.dst == 1 ? out : p->scratch;
-                e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s);
+                e = launch_pass(d, p->dtype, src, dst, p->tabs[i], s, pass_mods(p->flags, i, np, p->n));
                 if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
             }
         }
@@ -393,7 +441,7 @@ moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host
         const size_t cb = size_t(rows * p->n) * p->esize;
         if (!p->sub[0]) {
             for (int k = 0; k < 2; k++) {
-                moa_status_t st = moa_fft_plan(&p->sub[k], p->n, rows, p->dtype, 1);
+                moa_status_t st = moa_fft_plan_ex(&p->sub[k], p->n, rows, p->dtype, 1, p->flags);
                 if (st) return st;
                 e = cudaStreamCreateWithFlags(&p->ss[k], cudaStreamNonBlocking);
                 if (e != cudaSuccess) return cuda_fail(e, "exec_host stream");
@@ -557,6 +605,44 @@ moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64
     return MOA_OK;
 }
 
+moa_status_t moa_fft_output_index(moa_fft_plan_t p, int64_t *pos, int64_t count) {
+    if (!p || !pos) return fail(MOA_EINVAL, "output_index: null argument");
+    if (p->is3d) return fail(MOA_EUNSUPPORTED, "output_index: 1-D plans only");
+    if (count != p->n) return fail(MOA_EINVAL, "output_index: count must equal n");
+    const int64_t n = p->n;
+    if (p->dist) {
+        const int64_t P = p->ngpu, M = n / P;
+        const bool lifted = p->flags & MOA_FFT_LIFTED_ORDER;
+        for (int64_t k = 0; k < n; k++) pos[k] = lifted ? (k % P) * M + k / P : k;
+        return MOA_OK;
+    }
+    if (!p->lifted_out) {
+        for (int64_t k = 0; k < n; k++) pos[k] = k;
+        return MOA_OK;
+    }
+    // every (line, k) of the last pass of row 0: natural address -> lifted address
+    const moa_pass_desc_t &nat = p->natural_last, &lif = p->passes.back();
+    const int64_t R = int64_t(1) << nat.logR;
+    int64_t lines = 1;
+    for (int i = 0; i < nat.ndig; i++) lines *= nat.ext[i];
+    const int64_t row_lines = lines / p->batch;  // the batch digit is the slowest
+    for (int64_t l = 0; l < row_lines; l++) {
+        int64_t rem = l, na = 0, la = 0;
+        for (int i = 0; i < nat.ndig; i++) {
+            const int64_t d = rem % nat.ext[i];
+            rem /= nat.ext[i];
+            na += d * nat.out_str[i];
+            la += d * lif.out_str[i];
+        }
+        for (int64_t k = 0; k < R; k++) {
+            const int64_t a = na + k * nat.out_kstr;
+            if (a < 0 || a >= n) return fail(MOA_EINVAL, "output_index: descriptor out of range");
+            pos[a] = la + k * lif.out_kstr;
+        }
+    }
+    return MOA_OK;
+}
+
 moa_status_t moa_fft_plan_describe(moa_fft_plan_t p, moa_pass_desc_t *out, int max_passes, int *npasses) {
     if (!p || !out || !npasses) return fail(MOA_EINVAL, "plan_describe: null argument");
     if (int(p->passes.size()) > max_passes) return fail(MOA_EINVAL, "plan_describe: output array too small");
@@ -591,7 +677,9 @@ extern "C" moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, c
         if (st.kind == 0) {
             for (int r = 0; r < ngpu; r++) {
                 const moa_pass_desc_t &d = plans[r]->passes[st.pass];
-                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, d.dst), plans[r]->tabs[st.pass], s);
+                const PassMods mods = pass_mods(plans[r]->flags, size_t(st.pass), plans[r]->passes.size(), plans[r]->n);
+                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, d.dst), plans[r]->tabs[st.pass], s,
+                                            mods);
                 if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback pass: ") + cudaGetErrorString(e));
             }
         } else {

@@ -92,7 +92,7 @@ void dig(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, int64_t ts) {
 bool dist_ready(int ngpu) { return (g_comm || g_loopback) && g_ngpu == ngpu; }
 
 moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::vector<moa_pass_desc_t> &passes,
-                              std::vector<DistStep> &steps) {
+                              std::vector<DistStep> &steps, bool lifted_order) {
     passes.clear();
     steps.clear();
     const int64_t M = N / p, C = M / p;
@@ -116,6 +116,8 @@ moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::v
     // E2
     steps.push_back({1, -1, 2, 3, C});
     // B: the local length-M FFT; buffer ids remapped in -> 3, scratch -> out(1), out -> 2
+    // (lifted order: in -> 3, scratch -> 2, out -> 1 -- B writes the result,
+    // X[g + p k2] at offset k2, and E3 + the unpack are skipped)
     {
         std::vector<int64_t> rad;
         moa_status_t st = plan_radices(M, 1, dtype, rad);
@@ -123,7 +125,8 @@ moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::v
         std::vector<moa_pass_desc_t> b;
         st = psi_lift_passes(M, 1, dtype, rad.data(), int(rad.size()), b);
         if (st) return st;
-        const int remap[3] = {3, 2, 1};
+        const int remap_nat[3] = {3, 2, 1}, remap_lift[3] = {3, 1, 2};
+        const int *remap = lifted_order ? remap_lift : remap_nat;
         for (auto &d : b) {
             d.src = remap[d.src];
             d.dst = remap[d.dst];
@@ -131,6 +134,7 @@ moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::v
             passes.push_back(d);
         }
     }
+    if (lifted_order) return MOA_OK;
     // E3
     steps.push_back({1, -1, 2, 3, C});
     // U: out[k2_loc p + k1] = buf[k1][k2_loc]
@@ -203,14 +207,14 @@ moa_status_t dist_schedule_3d(int g, int p, int64_t n0, int64_t n1, int64_t n2, 
     return MOA_OK;
 }
 
-moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype) {
+moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype, bool lifted_order) {
     dp = new DistPlan;
     dp->rank = g_rank;
     dp->ngpu = g_ngpu;
     dp->loopback = g_loopback;
     dp->esize = dtype == MOA_C128 ? 16 : 8;
     dp->local_elems = n / g_ngpu;
-    moa_status_t st = dist_schedule_1d(g_rank, g_ngpu, n, dtype, dp->passes, dp->steps);
+    moa_status_t st = dist_schedule_1d(g_rank, g_ngpu, n, dtype, dp->passes, dp->steps, lifted_order);
     if (st) return st;
     cudaError_t e = cudaMalloc(&dp->scratch2, size_t(dp->local_elems) * dp->esize);
     if (e != cudaSuccess) {
@@ -246,7 +250,7 @@ int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes) {
 
 moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
                        moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
-                       cudaEvent_t *evs) {
+                       cudaEvent_t *evs, uint32_t flags, int64_t N) {
     if (dp->loopback) return fail(MOA_EINVAL, "dist: a loopback plan runs through moa_fft_exec_loopback");
     if (!g_comm) return fail(MOA_EINVAL, "dist: no communicator (moa_fft_dist_init)");
     void *bufs[4] = {const_cast<void *>(in), out, scratch, dp->scratch2};
@@ -255,7 +259,8 @@ moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes,
         if (evs) cudaEventRecord(evs[i], s);
         if (st.kind == 0) {
             const moa_pass_desc_t &d = passes[st.pass];
-            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[d.dst], tabs[st.pass], s);
+            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[d.dst], tabs[st.pass], s,
+                                        pass_mods(flags, size_t(st.pass), passes.size(), N));
             if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("dist pass: ") + cudaGetErrorString(e));
         } else {
             const size_t cnt = size_t(st.count) * 2;
@@ -332,7 +337,8 @@ moa_status_t moa_fft_dist_loopback(int rank, int ngpu) {
 // kinds[i] = 0 pass / 1 all-to-all; counts[i] = per-peer elements of an all-to-all.
 moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
                                void *passes_v, int max_passes, int *npasses, int32_t *kinds,
-                               int32_t *srcs, int32_t *dsts, int64_t *counts, int max_steps, int *nsteps) {
+                               int32_t *srcs, int32_t *dsts, int64_t *counts, int max_steps, int *nsteps,
+                               uint32_t flags) {
     moa_pass_desc_t *passes = static_cast<moa_pass_desc_t *>(passes_v);
     if (!passes || !npasses || !kinds || !srcs || !dsts || !counts || !nsteps)
         return fail(MOA_EINVAL, "dist_describe: null output");
@@ -346,7 +352,7 @@ moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t
         st = dist_schedule_3d(rank, ngpu, n0, n1, n2, dtype, ps, ss);
     } else {
         if (log2_exact(n0) < 0 || n0 < int64_t(ngpu) * ngpu) return fail(MOA_EUNSUPPORTED, "dist_describe: bad n");
-        st = dist_schedule_1d(rank, ngpu, n0, dtype, ps, ss);
+        st = dist_schedule_1d(rank, ngpu, n0, dtype, ps, ss, (flags & MOA_FFT_LIFTED_ORDER) != 0);
     }
     if (st) return st;
     if (int(ps.size()) > max_passes || int(ss.size()) > max_steps) return fail(MOA_EINVAL, "dist_describe: arrays too small");

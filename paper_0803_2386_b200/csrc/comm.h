@@ -35,18 +35,18 @@ struct DistPlan {
 };
 
 bool dist_ready(int ngpu);
-moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype);
+moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype, bool lifted_order = false);
 moa_status_t dist_plan_3d(DistPlan *&dp, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype);
 moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
                        moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
-                       cudaEvent_t *evs);
+                       cudaEvent_t *evs, uint32_t flags, int64_t N);
 void dist_plan_free(DistPlan *dp);
 int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes);
 
 // host-only construction of the distributed schedule for a given rank (used by
 // the planner and by the introspection / gloo tests)
 moa_status_t dist_schedule_1d(int rank, int ngpu, int64_t n, moa_dtype_t dtype, std::vector<moa_pass_desc_t> &passes,
-                              std::vector<DistStep> &steps);
+                              std::vector<DistStep> &steps, bool lifted_order = false);
 moa_status_t dist_schedule_3d(int rank, int ngpu, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype,
                               std::vector<moa_pass_desc_t> &passes, std::vector<DistStep> &steps);
 

@@ -136,6 +136,8 @@ struct KArgs {
     int32_t lf_load, lf_store;
     int32_t ring;     // 0: HBM both sides; 1: loads from the L2 ring; 2: stores to the ring
     int32_t discard;  // ring == 1: discard the consumed ring lines (no write-back)
+    int32_t conj_in, conj_out;  // inverse transform: conjugate loads / results (PassMods)
+    double scale;               // results times scale (1: none)
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -344,6 +346,14 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         }
     }
 
+    // ---- inverse / normalisation modifiers of the plan's last pass
+    if (a.conj_out || a.scale != 1.0) {
+        using T = typename RealOf<V>::type;
+        const T sr = T(a.scale), si = a.conj_out ? -T(a.scale) : T(a.scale);
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = mk<V>(pts[m].x * sr, pts[m].y * si);
+    }
+
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
     {
         const uint64_t pol = l2_policy(a.ring == 2);
@@ -376,6 +386,10 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
         const int64_t step = int64_t(TPL) * a.in_kstr;
 #pragma unroll
         for (int m = 0; m < P; m++) pts[m] = ld_pol(base + m * step, pol);
+    }
+    if (a.conj_in) {  // inverse transform: DFT of conj(x) (the plan's first pass)
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m].y = -pts[m].y;
     }
     tile_compute<V, LR>(a, line0, sm, ring_off, pts);
 }
@@ -537,8 +551,12 @@ const std::array<PFn<float2>, 36> kPair64 = make_pair_table<float2>(std::make_in
 const std::array<KFn<double2>, 13> kTab128 = make_table<double2>(std::make_integer_sequence<int, 13>{});
 const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
 
-KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines) {
+KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines,
+                const PassMods &mods) {
     KArgs a{};
+    a.conj_in = mods.conj_in;
+    a.conj_out = mods.conj_out;
+    a.scale = mods.scale;
     a.in = in;
     a.out = out;
     a.ndig = d.ndig;
@@ -574,9 +592,9 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
 
 template <typename V>
 cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
-                     const DevTables &tb, cudaStream_t stream) {
+                     const DevTables &tb, cudaStream_t stream, const PassMods &mods) {
     int64_t nlines = 0;
-    KArgs a = fill_args(d, in, out, tb, &nlines);
+    KArgs a = fill_args(d, in, out, tb, &nlines, mods);
     const int64_t tiles = nlines / d.W;
     KFn<V> fn = tab[d.logR];
     if (d.smem_bytes > 48 * 1024) {
@@ -590,11 +608,11 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
 template <typename V>
 cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc_t &dA, const moa_pass_desc_t &dB,
                           const void *in, void *out, const RingState &rs, const DevTables &tA, const DevTables &tB,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const PassMods &mA, const PassMods &mB) {
     int64_t nA = 0, nB = 0;
     PairArgs p{};
-    p.A = fill_args(dA, in, rs.ring, tA, &nA);
-    p.B = fill_args(dB, rs.ring, out, tB, &nB);
+    p.A = fill_args(dA, in, rs.ring, tA, &nA, mA);
+    p.B = fill_args(dB, rs.ring, out, tB, &nB, mB);
     p.TA = int32_t((nA / dA.W) / dA.ring_groups);
     p.TB = int32_t((nB / dB.W) / dB.ring_groups);
     p.groups = dA.ring_groups;
@@ -627,18 +645,19 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
 }  // namespace
 
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const PassMods &mods) {
     if (d.logR < 0 || d.logR > 12) return cudaErrorInvalidValue;
-    if (dtype == MOA_C128) return launch_t<double2>(kTab128, d, in, out, tab, stream);
-    return launch_t<float2>(kTab64, d, in, out, tab, stream);
+    if (dtype == MOA_C128) return launch_t<double2>(kTab128, d, in, out, tab, stream, mods);
+    return launch_t<float2>(kTab64, d, in, out, tab, stream, mods);
 }
 
 cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
-                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream) {
+                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream,
+                        const PassMods &mA, const PassMods &mB) {
     if (dA.logR < 5 || dA.logR > 10 || dB.logR < 5 || dB.logR > 10 || dA.threads != dB.threads)
         return cudaErrorInvalidValue;
-    if (dtype == MOA_C128) return launch_pair_t<double2>(kPair128, dA, dB, in, out, rs, tA, tB, stream);
-    return launch_pair_t<float2>(kPair64, dA, dB, in, out, rs, tA, tB, stream);
+    if (dtype == MOA_C128) return launch_pair_t<double2>(kPair128, dA, dB, in, out, rs, tA, tB, stream, mA, mB);
+    return launch_pair_t<float2>(kPair64, dA, dB, in, out, rs, tA, tB, stream, mA, mB);
 }
 
 cudaError_t kernel_attributes(moa_dtype_t dtype, int logR, int *max_threads, int *regs) {

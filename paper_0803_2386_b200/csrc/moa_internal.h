@@ -49,11 +49,24 @@ struct RingState {
     unsigned long long epoch = 0;         // execs of this pair so far
     unsigned long long *stats = nullptr;  // MOA_FFT_STATS=1: B waits/spins/cycles, A waits/spins/cycles
 };
+// Per-launch modifiers of a pass (plan flags, include/moa_fft.h): the inverse
+// transform as conj(DFT(conj(x))) -- conjugate the first pass's loads and the
+// last pass's results -- and the 1/N normalisation folded into the last
+// pass's store (exact: N is a power of two).
+struct PassMods {
+    int conj_in = 0;
+    int conj_out = 0;
+    double scale = 1.0;
+};
+// the modifiers of pass i of npass under `flags` (MOA_FFT_INVERSE / _NORMALIZE)
+PassMods pass_mods(uint32_t flags, size_t i, size_t npass, int64_t N);
+
 int log2_exact(int64_t n);
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out,
-                        const DevTables &tab, cudaStream_t stream);
+                        const DevTables &tab, cudaStream_t stream, const PassMods &mods = PassMods());
 cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
-                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream);
+                        void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream,
+                        const PassMods &mA = PassMods(), const PassMods &mB = PassMods());
 // psi.cpp: fuse the passes of a one-GPU lifting into L2-staged pairs where the
 // group working set fits (marks ring fields; returns how many pairs were made)
 int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,

@@ -57,6 +57,10 @@ def test_other_argument_errors():
     with pytest.raises(m.MoaError):
         m.moa_psi_describe(64, 1, "c128", [8, 3, 3])
     assert m.lib.moa_fft_destroy(None) == m.MOA_OK
+    # plan flags: unknown bits, lifted order on a 3-D plan
+    assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 1, 8) == m.MOA_EINVAL
+    assert m.lib.moa_fft_plan_3d_ex(ctypes.byref(h), 8, 8, 8, 1, 1, m.MOA_FFT_LIFTED_ORDER) == m.MOA_EUNSUPPORTED
+    assert m.lib.moa_fft_output_index(None, None, 0) == m.MOA_EINVAL
 
 
 def test_planner_liftings():
@@ -134,6 +138,22 @@ def test_dist_1d_schedule_host_simulation(p):
     ref = oracle.fft_radix2(x)
     got = np.concatenate(outs)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_1d_lifted_order_schedule(p):
+    # MOA_FFT_LIFTED_ORDER: no third all-to-all, no unpack; rank g holds X[g + p k2]
+    # at offset k2 -- the final transpose is never executed
+    N = 1 << 12
+    x = synth.fill(N, 9, synth.UNIFORM)
+    sch = [m.moa_dist_describe(r, p, N, "c128", flags=m.MOA_FFT_LIFTED_ORDER) for r in range(p)]
+    kinds = [s[0] for s in sch[0]["steps"]]
+    assert kinds.count("alltoall") == 2
+    outs = run_dist(sch, np.split(x, p))
+    ref = oracle.fft_radix2(x)
+    for g in range(p):
+        want = ref[g::p]
+        assert np.linalg.norm(outs[g] - want) / np.linalg.norm(want) < 1e-12
 
 
 @pytest.mark.parametrize("p", [2, 4, 8])
