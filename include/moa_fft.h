@@ -51,7 +51,7 @@ typedef enum { MOA_C64 = 0, MOA_C128 = 1 } moa_dtype_t;
 typedef struct moa_fft_plan_s *moa_fft_plan_t; /* opaque, library-owned */
 
 #define MOA_MAX_DIGITS 6
-#define MOA_MAX_PASSES 16
+#define MOA_MAX_PASSES 36
 
 /*
  * moa_fft_plan -- plan `batch` independent forward transforms of length n.
@@ -103,11 +103,18 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
  *                        holds X[g + p k2] at offset k2 (the rank is the fastest
  *                        output digit).  A plan may keep natural order (identity
  *                        map) where that costs nothing extra (single-pass plans).
- * Unknown bits -> MOA_EINVAL; LIFTED_ORDER on a 3-D plan -> MOA_EUNSUPPORTED.
+ * Unknown bits -> MOA_EINVAL; LIFTED_ORDER or UNBLOCKED on a 3-D plan, UNBLOCKED
+ * with ngpu > 1 or with LIFTED_ORDER -> MOA_EUNSUPPORTED.
  */
 #define MOA_FFT_INVERSE 1u
 #define MOA_FFT_NORMALIZE 2u
 #define MOA_FFT_LIFTED_ORDER 4u
+/* MOA_FFT_UNBLOCKED (1-D, ngpu = 1; an ablation): the paper's unblocked control
+ * ("c >= n disables blocking"), i.e. Van Loan's program as
+ * written (Fig. vanloan_fft): x <- P_n x, then for q = 1..t one
+ * global radix-2 stage per pass (t + 1 HBM round trips instead of the
+ * lifting's few).  Combines with INVERSE / NORMALIZE, not with LIFTED_ORDER. */
+#define MOA_FFT_UNBLOCKED 8u
 
 /* moa_fft_plan / moa_fft_plan_3d with flags (0 = the forward, natural-order plan). */
 moa_status_t moa_fft_plan_ex(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,
@@ -228,7 +235,10 @@ typedef struct {
     int64_t tw_off;             /* added to the line's exponent base (rank offset; 0 on one GPU) */
     int32_t out_ksplit;         /* store: k = khi*2^out_ksplit + klo, address += klo*out_kstr + khi*out_kstr_hi */
     int64_t out_kstr_hi;
-    int32_t nodft;              /* 1: identity (a pure data-movement pass) */
+    int32_t kind;               /* 0: lifted DFT pass (the ONF above); 1: identity (a pure data-
+                                 * movement pass); 2: one global radix-2 stage of the unblocked
+                                 * control (Van Loan, L = 2 in_kstr, in place); 3: the bit
+                                 * reversal P_n of every row (MOA_FFT_UNBLOCKED plans) */
     int32_t lf_load, lf_store;  /* 1: that side is coalesced along the lines (digit 0) */
     int32_t W;                  /* lines per CTA tile */
     int32_t threads;            /* CTA size */

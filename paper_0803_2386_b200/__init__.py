@@ -15,9 +15,9 @@ _SO = os.path.join(_HERE, "libmoafft.so")
 
 MOA_OK, MOA_EINVAL, MOA_ENOMEM, MOA_ECUDA, MOA_ENCCL, MOA_EUNSUPPORTED = range(6)
 MOA_C64, MOA_C128 = 0, 1
-MOA_FFT_INVERSE, MOA_FFT_NORMALIZE, MOA_FFT_LIFTED_ORDER = 1, 2, 4
+MOA_FFT_INVERSE, MOA_FFT_NORMALIZE, MOA_FFT_LIFTED_ORDER, MOA_FFT_UNBLOCKED = 1, 2, 4, 8
 MAX_DIGITS = 6
-MAX_PASSES = 16
+MAX_PASSES = 36
 STATUS_NAMES = {0: "MOA_OK", 1: "MOA_EINVAL", 2: "MOA_ENOMEM", 3: "MOA_ECUDA", 4: "MOA_ENCCL",
                 5: "MOA_EUNSUPPORTED"}
 
@@ -41,7 +41,7 @@ class PassDesc(ctypes.Structure):
         ("in_kstr", ctypes.c_int64), ("out_kstr", ctypes.c_int64),
         ("twN", ctypes.c_int64), ("tw_off", ctypes.c_int64),
         ("out_ksplit", ctypes.c_int32), ("out_kstr_hi", ctypes.c_int64),
-        ("nodft", ctypes.c_int32),
+        ("kind", ctypes.c_int32),
         ("lf_load", ctypes.c_int32), ("lf_store", ctypes.c_int32),
         ("W", ctypes.c_int32), ("threads", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
         ("line_pad", ctypes.c_int32), ("src", ctypes.c_int32), ("dst", ctypes.c_int32),
@@ -55,7 +55,7 @@ class PassDesc(ctypes.Structure):
                     in_str=list(self.in_str[:nd]), out_str=list(self.out_str[:nd]),
                     tw_str=list(self.tw_str[:nd]), in_kstr=self.in_kstr, out_kstr=self.out_kstr,
                     twN=self.twN, tw_off=self.tw_off, out_ksplit=self.out_ksplit,
-                    out_kstr_hi=self.out_kstr_hi, nodft=self.nodft, lf_load=self.lf_load,
+                    out_kstr_hi=self.out_kstr_hi, kind=self.kind, lf_load=self.lf_load,
                     lf_store=self.lf_store, W=self.W, threads=self.threads,
                     smem_bytes=self.smem_bytes, line_pad=self.line_pad, src=self.src, dst=self.dst,
                     ring=self.ring, ring_slots=self.ring_slots, ring_lag=self.ring_lag,
@@ -288,9 +288,10 @@ class FFTPlan:
     torch device tensors (complex64 / complex128, contiguous)."""
 
     def __init__(self, n: int = 0, batch: int = 1, dtype="c128", ngpu: int = 1, radices=None, _handle=None,
-                 inverse: bool = False, normalize: bool = False, lifted_order: bool = False):
+                 inverse: bool = False, normalize: bool = False, lifted_order: bool = False,
+                 unblocked: bool = False):
         flags = (MOA_FFT_INVERSE if inverse else 0) | (MOA_FFT_NORMALIZE if normalize else 0) | \
-            (MOA_FFT_LIFTED_ORDER if lifted_order else 0)
+            (MOA_FFT_LIFTED_ORDER if lifted_order else 0) | (MOA_FFT_UNBLOCKED if unblocked else 0)
         if _handle is not None:
             self.h = _handle
         elif radices is not None:

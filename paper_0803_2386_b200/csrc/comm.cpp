@@ -144,7 +144,7 @@ moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::v
         dig(d, C, 1, p, 0);
         d.in_kstr = C;
         d.out_kstr = 1;
-        d.nodft = 1;
+        d.kind = 1;
         d.lf_load = 1;
         d.lf_store = 0;
         d.src = 3;

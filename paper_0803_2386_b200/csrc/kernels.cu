@@ -131,7 +131,7 @@ struct KArgs {
     int32_t twh;     // split bit of the two-level table
     int32_t ksplit;  // store: k = khi 2^ksplit + klo
     int64_t out_kstr_hi;
-    int32_t nodft;
+    int32_t nodft;  // moa_pass_desc_t kind == 1
     int32_t W, LS;   // lines per tile, smem line stride (elements)
     int32_t lf_load, lf_store;
     int32_t ring;     // 0: HBM both sides; 1: loads from the L2 ring; 2: stores to the ring
@@ -536,6 +536,74 @@ __global__ void __launch_bounds__(512) pair_kernel(const __grid_constant__ PairA
     }
 }
 
+// ---------------------------------------------------------------------------
+// The unblocked control (MOA_FFT_UNBLOCKED): Van Loan's program as written,
+// Fig. vanloan_fft P:1845-1876 -- x <- P_n x, then for q = 1..t one global
+// radix-2 stage x_{L x r} <- B_L x_{L x r} (L = 2^q), each a full HBM round
+// trip.  Butterfly of Fig. fftpsirad2: c = w(row) x(col'+row+L/2),
+// d = x(col'+row), x(col'+row) = d + c, x(col'+row+L/2) = d - c, with
+// w(row) = w_L^row = w_n^{row n/L} from the two-level table.
+template <typename V>
+__global__ void __launch_bounds__(256) vl_stage_kernel(V *__restrict__ x, int64_t half_total, int logh, int64_t n,
+                                                       const double2 *__restrict__ hi, const double2 *__restrict__ lo,
+                                                       int twh, int conj_out, double scale) {
+    const int64_t h = int64_t(1) << logh;
+    const int64_t estep = n >> (logh + 1);  // n / L
+    using T = typename RealOf<V>::type;
+    const T sr = T(scale), si = conj_out ? -T(scale) : T(scale);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < half_total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = i & (h - 1);
+        const int64_t top = ((i >> logh) << (logh + 1)) + row;  // col' + row (blocks of L never straddle rows)
+        const V d = x[top], b = x[top + h];
+        const V w = cvt_tw(tw_lookup(hi, lo, (row * estep) & (n - 1), twh), V{});
+        const V c = cmul(b, w);
+        V u = cadd(d, c), v = csub(d, c);
+        if (conj_out || scale != 1.0) {
+            u = mk<V>(u.x * sr, u.y * si);
+            v = mk<V>(v.x * sr, v.y * si);
+        }
+        x[top] = u;
+        x[top + h] = v;
+    }
+}
+
+// P_n of every row (Fig. vanloan_fft line 1): out[b n + i] = in[b n + bitrev_t(i)]
+template <typename V>
+__global__ void __launch_bounds__(256) bitrev_kernel(const V *__restrict__ in, V *__restrict__ out, int64_t total, int t,
+                                                     int conj_in) {
+    const int64_t mask = (int64_t(1) << t) - 1;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = i & mask;
+        const int64_t src = (i & ~mask) | (t ? int64_t(__brevll((unsigned long long)j) >> (64 - t)) : 0);
+        V v = in[src];
+        if (conj_in) v.y = -v.y;
+        out[i] = v;
+    }
+}
+
+template <typename V>
+cudaError_t launch_unblocked(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb,
+                             cudaStream_t stream, const PassMods &mods, int64_t total) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t work = d.kind == 2 ? total / 2 : total;
+    int64_t grid = (work + 255) / 256;
+    if (grid > int64_t(sms) * 16) grid = int64_t(sms) * 16;
+    if (grid < 1) grid = 1;
+    if (d.kind == 3) {
+        bitrev_kernel<V><<<unsigned(grid), 256, 0, stream>>>(static_cast<const V *>(in), static_cast<V *>(out), total,
+                                                              log2_exact(d.twN), mods.conj_in);
+    } else {
+        const int lN = log2_exact(d.twN);
+        vl_stage_kernel<V><<<unsigned(grid), 256, 0, stream>>>(static_cast<V *>(out), work, log2_exact(d.in_kstr), d.twN,
+                                                               static_cast<const double2 *>(tb.tw_hi),
+                                                               static_cast<const double2 *>(tb.tw_lo), (lN + 1) / 2,
+                                                               mods.conj_out, mods.scale);
+    }
+    return cudaGetLastError();
+}
+
 template <typename V> using KFn = void (*)(const KArgs);
 template <typename V> using PFn = void (*)(const PairArgs);
 
@@ -580,7 +648,7 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.tw_off = d.tw_off;
     a.ksplit = d.out_ksplit < d.logR ? d.out_ksplit : 30;
     a.out_kstr_hi = d.out_kstr_hi;
-    a.nodft = d.nodft;
+    a.nodft = d.kind == 1;
     a.W = d.W;
     a.LS = (1 << d.logR) + d.line_pad;
     a.lf_load = d.lf_load;
@@ -646,6 +714,11 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
 
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
                         cudaStream_t stream, const PassMods &mods) {
+    if (d.kind == 2 || d.kind == 3) {  // the unblocked control: total elements = ext[0] (rows * n)
+        const int64_t total = d.ndig ? d.ext[0] : 1;
+        if (dtype == MOA_C128) return launch_unblocked<double2>(d, in, out, tab, stream, mods, total);
+        return launch_unblocked<float2>(d, in, out, tab, stream, mods, total);
+    }
     if (d.logR < 0 || d.logR > 12) return cudaErrorInvalidValue;
     if (dtype == MOA_C128) return launch_t<double2>(kTab128, d, in, out, tab, stream, mods);
     return launch_t<float2>(kTab64, d, in, out, tab, stream, mods);

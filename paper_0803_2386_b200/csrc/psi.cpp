@@ -67,7 +67,10 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // (point-contiguous lines of >= 2^10 points: one line per CTA -- more, smaller
     // CTAs per SM overlap their load and compute phases better; measured cfg5
     // z-pass 7.48 -> 6.84 ms)
-    int64_t W = lf ? slots : (TPL >= 64 ? 1 : 256 / TPL);
+    // (line-coalesced passes of short lines -- R < 128, e.g. the p-point pass of
+    // the processor lifting or an all-radix-2 lifting -- take more lines so a
+    // CTA has at least 128 threads)
+    int64_t W = lf ? (TPL >= 8 ? slots : (slots > 128 / TPL ? slots : 128 / TPL)) : (TPL >= 64 ? 1 : 256 / TPL);
     // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
     // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
     // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
@@ -207,7 +210,7 @@ int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t
 moa_status_t psi_lift_passes(int64_t n, int64_t batch, moa_dtype_t dtype, const int64_t *radices, int nrad,
                              std::vector<moa_pass_desc_t> &out) {
     out.clear();
-    if (nrad < 1 || nrad > MOA_MAX_PASSES) return fail(MOA_EINVAL, "psi: lifting must have 1..16 factors");
+    if (nrad < 1 || nrad > MOA_MAX_PASSES) return fail(MOA_EINVAL, "psi: lifting must have 1..MOA_MAX_PASSES factors");
     int64_t prod = 1;
     for (int i = 0; i < nrad; i++) {
         int lr = log2_exact(radices[i]);
@@ -502,7 +505,10 @@ static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, con
     d.dst = 1;
     ring(d, 1, g23, G23);
     out.push_back(d);
-    for (auto &x : out) psi_choose_tile(x, dtype);
+    for (auto &x : out) {  // the group structure needs tiles of exactly W lines
+        psi_choose_tile(x, dtype);
+        if (x.W != W && tile_ok(x, dtype, W)) set_tile(x, dtype, W);
+    }
     // both passes of a pair need one CTA size: widen the narrower tile
     for (int p = 0; p < 4; p += 2) {
         moa_pass_desc_t &A = out[p], &B = out[p + 1];

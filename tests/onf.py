@@ -59,7 +59,7 @@ def run_pass(d, src, dst, lines_sel=None, enum=None):
         load, store, tw = load[lines_sel], store[lines_sel], tw[lines_sel]
     R = d["R"]
     lines = src[load]
-    if not d["nodft"]:
+    if not d["kind"]:
         F = np.exp(-2j * np.pi * np.outer(np.arange(R), np.arange(R)) / R)
         lines = lines @ F.T
     if d["twN"] > 1:

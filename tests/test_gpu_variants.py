@@ -135,3 +135,18 @@ def test_exec_host_inverse(m, torch_cuda):
     plan.exec_host(hin, hout)
     ref = oracle.fft_radix2_rows_sign(x, n, +1) / n
     assert rel_l2(hout.numpy(), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,batch", [(1, 2), (2, 3), (1 << 10, 2), (1 << 17, 1)])
+def test_unblocked_control(m, torch_cuda, dtype, n, batch):
+    # the paper's unblocked control: P_n then t global radix-2 stages
+    x = synth.fill(n * batch, 101, synth.UNIFORM, dtype)
+    plan = m.FFTPlan(n, batch, dtype, unblocked=True)
+    d = plan.describe()
+    assert [p["kind"] for p in d] == [3] + [2] * (n.bit_length() - 1)
+    y = run(torch_cuda, plan, x).astype(np.complex128)
+    assert rel_l2(y, oracle.fft_radix2_rows(x.astype(np.complex128), n)) <= TOL[dtype]
+    inv = m.FFTPlan(n, batch, dtype, unblocked=True, inverse=True, normalize=True)
+    z = run(torch_cuda, inv, x).astype(np.complex128)
+    assert rel_l2(z, oracle.fft_radix2_rows_sign(x.astype(np.complex128), n, +1) / n) <= TOL[dtype]
