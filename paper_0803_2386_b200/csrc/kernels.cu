@@ -570,14 +570,15 @@ __global__ void __launch_bounds__(256) vl_stage_kernel(V *__restrict__ x, int64_
 // P_n of every row (Fig. vanloan_fft line 1): out[b n + i] = in[b n + bitrev_t(i)]
 template <typename V>
 __global__ void __launch_bounds__(256) bitrev_kernel(const V *__restrict__ in, V *__restrict__ out, int64_t total, int t,
-                                                     int conj_in) {
+                                                     int conj_in, int conj_out, double scale) {
     const int64_t mask = (int64_t(1) << t) - 1;
+    using T = typename RealOf<V>::type;
+    const T sr = T(scale), si = (conj_in != conj_out) ? -T(scale) : T(scale);  // n = 1: first and last pass
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t j = i & mask;
         const int64_t src = (i & ~mask) | (t ? int64_t(__brevll((unsigned long long)j) >> (64 - t)) : 0);
-        V v = in[src];
-        if (conj_in) v.y = -v.y;
-        out[i] = v;
+        const V v = in[src];
+        out[i] = mk<V>(v.x * sr, v.y * si);
     }
 }
 
@@ -593,7 +594,7 @@ cudaError_t launch_unblocked(const moa_pass_desc_t &d, const void *in, void *out
     if (grid < 1) grid = 1;
     if (d.kind == 3) {
         bitrev_kernel<V><<<unsigned(grid), 256, 0, stream>>>(static_cast<const V *>(in), static_cast<V *>(out), total,
-                                                              log2_exact(d.twN), mods.conj_in);
+                                                              log2_exact(d.twN), mods.conj_in, mods.conj_out, mods.scale);
     } else {
         const int lN = log2_exact(d.twN);
         vl_stage_kernel<V><<<unsigned(grid), 256, 0, stream>>>(static_cast<V *>(out), work, log2_exact(d.in_kstr), d.twN,
