@@ -279,6 +279,88 @@ moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, 
         if (l < 0 || l > 12) return fail(MOA_EINVAL, "psi: 3-D extents must be powers of two <= 4096");
     }
     const int64_t plane = n1 * n2, vol = n0 * plane;
+    // Layout choice (measured): complex128 uses the rotating
+    // layouts (cfg5 22.5 -> 19.4 ms); complex64 the in-place axis passes (equal
+    // time, no scratch).  MOA_FFT_3D_ROT = 0 / 1 / 2 overrides (ablations).
+    const char *rot_env = std::getenv("MOA_FFT_3D_ROT");
+    const char rot = rot_env && *rot_env ? rot_env[0] : (dtype == MOA_C128 ? '2' : '0');
+    if (rot == '2' && howmany == 1 && n0 > 1 && n1 > 1 && n2 > 1) {
+        // Rotating layouts, axis order z, x, y: every pass reads contiguous
+        // lines and stores transposed so the next axis becomes contiguous (the
+        // strided side is always a store, merged into full lines in L2); every
+        // store stride is one row (n0, n1 or n2 elements), never a plane:
+        //   in [x][y][z] --z--> out [y][z][x] --x--> scratch [z][x][y] --y--> out [x][y][z]
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n2));  // z: line (x, y), k_z -> out[y][k_z][x]
+        add_digit(d, n0, plane, 1, 0);
+        add_digit(d, n1, n2, n2 * n0, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n0;
+        d.lf_store = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n0));  // x: line (y, z) of [y][z][x], k_x -> scratch[z][k_x][y]
+        add_digit(d, n1, n2 * n0, 1, 0);
+        add_digit(d, n2, n0, n0 * n1, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n1;
+        d.lf_store = 1;
+        d.src = 1;
+        d.dst = 2;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n1));  // y: line (z, x) of [z][x][y], k_y -> out[x][k_y][z]
+        add_digit(d, n2, n0 * n1, 1, 0);
+        add_digit(d, n0, n1, plane, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n2;
+        d.lf_store = 1;
+        d.src = 2;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        return MOA_OK;
+    }
+    if (rot == '1' && howmany == 1 && n0 > 1 && n1 > 1 && n2 > 1) {
+        // Rotating layouts: every pass reads contiguous lines and stores
+        // transposed so the next axis becomes contiguous (the strided side is
+        // always a store, which the L2 merges into full lines):
+        //   in  [x][y][z] --z--> out [x][z][y] --y--> scratch [z][y][x] --x--> out [x][y][z]
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n2));  // z: line (y, x), k_z -> out[x][k_z][y]
+        add_digit(d, n1, n2, 1, 0);
+        add_digit(d, n0, plane, plane, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n1;
+        d.lf_store = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n1));  // y: line (x, z) of [x][z][y], k_y -> scratch[z][k_y][x]
+        add_digit(d, n0, plane, 1, 0);
+        add_digit(d, n2, n1, n1 * n0, 0);
+        d.in_kstr = 1;
+        d.out_kstr = n0;
+        d.lf_store = 1;
+        d.src = 1;
+        d.dst = 2;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n0));  // x: line (z, y) of [z][y][x], k_x -> out[k_x][y][z]
+        add_digit(d, n2, n1 * n0, 1, 0);
+        add_digit(d, n1, n0, n2, 0);
+        d.in_kstr = 1;
+        d.out_kstr = plane;
+        d.lf_store = 1;
+        d.src = 2;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        return MOA_OK;
+    }
     // axis 2: contiguous lines
     {
         moa_pass_desc_t d;

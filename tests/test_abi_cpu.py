@@ -117,8 +117,26 @@ def test_planner_descriptors_compute_the_dft(n, batch, dtype):
             assert d["ext"][0] % d["W"] == 0
 
 
+@pytest.mark.parametrize("rot", ["0", "1", "2"])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_psi_3d_layouts(monkeypatch, rot, dtype):
+    # in-place axis passes (0) and the two rotating-layout schedules (1: z,y,x;
+    # 2: z,x,y -- every pass reads contiguous lines, stores transposed)
+    monkeypatch.setenv("MOA_FFT_3D_ROT", rot)
+    for shape in [(8, 4, 16), (2, 32, 4), (16, 32, 64), (64, 8, 2)]:
+        passes = m.moa_psi_describe_3d(*shape, dtype=dtype)
+        if rot != "0":
+            assert all(d["lf_load"] == 0 for d in passes)          # contiguous loads only
+            assert [d["dst"] for d in passes][-1] == 1
+        x = synth.fill(int(np.prod(shape)), 7, synth.NORMAL)
+        got = run_plan(passes, x).reshape(shape)
+        ref = oracle.fft3d(x.reshape(shape))
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
 def test_psi_3d_descriptors(monkeypatch):
     monkeypatch.setenv("MOA_FFT_FUSE", "1")
+    monkeypatch.setenv("MOA_FFT_3D_ROT", "0")
     for shape in [(8, 4, 16), (16, 16, 16), (2, 32, 4), (64, 64, 64), (16, 32, 64)]:
         passes = m.moa_psi_describe_3d(*shape)
         if min(shape[1:]) >= 32 and shape[0] >= 8:

@@ -180,9 +180,10 @@ def test_exec_host_e2e(m, torch_cuda):
 # ---------------------------------------------------------------- 3-D
 @pytest.mark.parametrize("shape", [(8, 8, 8), (4, 16, 32), (64, 32, 16), (2, 2, 2), (1, 8, 4), (128, 128, 128)])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
-@pytest.mark.parametrize("fuse", ["", "1"])
-def test_3d(m, torch_cuda, monkeypatch, shape, dtype, fuse):
+@pytest.mark.parametrize("fuse,rot", [("", ""), ("1", "0"), ("", "0"), ("", "1"), ("", "2")])
+def test_3d(m, torch_cuda, monkeypatch, shape, dtype, fuse, rot):
     monkeypatch.setenv("MOA_FFT_FUSE", fuse)
+    monkeypatch.setenv("MOA_FFT_3D_ROT", rot)
     N = int(np.prod(shape))
     x = synth.fill(N, 13, synth.NORMAL, dtype)
     plan = m.FFTPlan.plan_3d(*shape, dtype=dtype)
