@@ -75,9 +75,12 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
     // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
     // one CTA per SM (measured: cfg5 x-pass 11.7 -> 9.3 ms).
-    const int64_t kbytes = (d.in_kstr > d.out_kstr ? d.in_kstr : d.out_kstr) * esize;
     const char *cap_env = std::getenv("MOA_FFT_SMEM_CAP");
-    const int64_t smem_cap = cap_env ? std::atoll(cap_env) : (lf && kbytes >= (int64_t(1) << 20) ? 200000 : 100 * 1024);
+    // (only a strided LOAD side needs the long runs: strided stores are merged
+    // into full lines in L2 -- tools/stride_bench, the rotating 3-D layouts)
+    const int64_t kload = d.in_kstr * esize;
+    const int64_t smem_cap = cap_env ? std::atoll(cap_env)
+                                     : (d.lf_load && kload >= (int64_t(1) << 20) ? 200000 : 100 * 1024);
     // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
     const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
     if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
