@@ -291,8 +291,10 @@ def main():
     if partitioned:
         sched = m.moa_dist_describe(rank, world, w["shape"] if w["kind"] == "3d" else w["n"], w["dtype"])
         for s in sched["steps"]:
-            if s[0] == "pass":
-                launches_l.append(("pass", f"pass_kernel<{vt},{sched['passes'][s[1]]['logR']}>"))
+            if s[0] in ("pass", "fused"):   # fused: the all-to-all done by the pass's NVLink stores
+                launches_l.append((s[0], f"pass_kernel<{vt},{sched['passes'][s[1]]['logR']}>"))
+            elif s[0] == "barrier":
+                launches_l.append(("barrier", "ncclAllReduce(1)"))
             else:
                 launches_l.append(("alltoall", "ncclAlltoAll"))
     else:
@@ -306,7 +308,9 @@ def main():
                 i += 1
     kinds = [k for k, _ in launches_l]
     per_step = [s / max(nexec, 1) for s in step_ms_list]
-    pass_idx = [i for i, k in enumerate(kinds) if k != "alltoall"]
+    pass_idx = [i for i, k in enumerate(kinds) if k in ("pass", "pair")]
+    if not pass_idx:
+        pass_idx = [i for i, k in enumerate(kinds) if k == "fused"]
     dom = max(pass_idx, key=lambda i: per_step[i])
     dom_ms = per_step[dom]
     dom_bytes = 2 * data_bytes                   # one HBM round trip of the local array per launch

@@ -199,9 +199,12 @@ moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, const void *
 
 /*
  * The distributed schedule of one rank (host only): passes[] as below; steps
- * i < nsteps are kinds[i] = 0 (run passes[srcs[i]]) or 1 (all-to-all of
+ * i < nsteps are kinds[i] = 0 (run passes[srcs[i]]), 1 (all-to-all of
  * counts[i] complex elements per peer from buffer srcs[i] to dsts[i]; buffer
- * ids 0 in, 1 out, 2 scratch, 3 scratch2).  is3d = 0: n0 is the 1-D length.
+ * ids 0 in, 1 out, 2 scratch, 3 scratch2), 2 (run passes[srcs[i]] with the
+ * following all-to-all fused into its stores: send-layout chunk h goes straight
+ * to rank h's buffer dsts[i] at offset rank * counts[i], over NVLink) or
+ * 3 (barrier).  Fusion is on unless MOA_FFT_PEER=0.  is3d = 0: n0 is the 1-D length.
  * flags: MOA_FFT_LIFTED_ORDER selects the 1-D schedule without the third
  * all-to-all and the unpack (other bits do not change the schedule).
  */

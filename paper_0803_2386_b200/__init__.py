@@ -277,8 +277,12 @@ def moa_dist_describe(rank: int, ngpu: int, n, dtype="c128", flags: int = 0) -> 
     for i in range(ns.value):
         if kinds[i] == 0:
             steps.append(("pass", srcs[i]))
-        else:
+        elif kinds[i] == 1:
             steps.append(("alltoall", srcs[i], dsts[i], counts[i]))
+        elif kinds[i] == 2:
+            steps.append(("fused", srcs[i], dsts[i], counts[i]))      # pass + all-to-all by its stores
+        else:
+            steps.append(("barrier",))
     return dict(passes=[passes[i].to_dict() for i in range(np_.value)], steps=steps)
 
 

@@ -326,6 +326,10 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
         if (!st && (flags & MOA_FFT_LIFTED_ORDER)) make_lifted_order(p);
     }
     if (!st) st = finish_plan(p);
+    if (!st && p->dist) {
+        st = dist_finish(p->dist, p->scratch);
+        if (!st) p->passes = p->dist->passes;
+    }
     if (st) {
         std::string msg = moa_fft_last_error();
         moa_fft_destroy(p);
@@ -399,6 +403,10 @@ moa_status_t moa_fft_plan_3d_ex(moa_fft_plan_t *plan, int64_t n0, int64_t n1, in
         if (!st) psi_fuse_3d(p->passes, dtype);
     }
     if (!st) st = finish_plan(p);
+    if (!st && p->dist) {
+        st = dist_finish(p->dist, p->scratch);
+        if (!st) p->passes = p->dist->passes;
+    }
     if (st) {
         std::string msg = moa_fft_last_error();
         moa_fft_destroy(p);
@@ -704,12 +712,19 @@ extern "C" moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, c
     };
     const auto &steps = plans[0]->dist->steps;
     for (const auto &st : steps) {
-        if (st.kind == 0) {
+        if (st.kind == 3) continue;  // barrier: the lock-step launch order already provides it
+        if (st.kind == 0 || st.kind == 2) {
             for (int r = 0; r < ngpu; r++) {
                 const moa_pass_desc_t &d = plans[r]->passes[st.pass];
-                const PassMods mods = pass_mods(plans[r]->flags, size_t(st.pass), plans[r]->passes.size(), plans[r]->n);
-                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, d.dst), plans[r]->tabs[st.pass], s,
-                                            mods);
+                PassMods mods = pass_mods(plans[r]->flags, size_t(st.pass), plans[r]->passes.size(), plans[r]->n);
+                if (st.kind == 2) {  // fused exchange: stores straight into every virtual rank's buffer
+                    mods.npeers = ngpu;
+                    for (int h = 0; h < ngpu; h++) mods.peers[h] = bufs(h, st.dst);
+                    mods.log_chunk = log2_exact(st.count);
+                    mods.self_off = int64_t(r) * st.count;
+                }
+                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, st.kind == 2 ? st.dst : d.dst),
+                                            plans[r]->tabs[st.pass], s, mods);
                 if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback pass: ") + cudaGetErrorString(e));
             }
         } else {

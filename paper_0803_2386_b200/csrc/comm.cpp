@@ -35,6 +35,8 @@ struct Nccl {
     decltype(&::ncclCommDestroy) commDestroy = nullptr;
     decltype(&::ncclCommAbort) commAbort = nullptr;
     decltype(&::ncclAlltoAll) alltoAll = nullptr;
+    decltype(&::ncclAllGather) allGather = nullptr;
+    decltype(&::ncclAllReduce) allReduce = nullptr;
     decltype(&::ncclGetErrorString) errStr = nullptr;
 };
 Nccl g_nccl;
@@ -55,6 +57,8 @@ moa_status_t load_nccl() {
     g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.commAbort = (decltype(g_nccl.commAbort))dlsym(h, "ncclCommAbort");
     g_nccl.alltoAll = (decltype(g_nccl.alltoAll))dlsym(h, "ncclAlltoAll");
+    g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+    g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
     g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
     if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.alltoAll)
         return fail(MOA_ENCCL, "NCCL: the loaded library lacks ncclAlltoAll (needs NCCL >= 2.28)");
@@ -90,6 +94,130 @@ void dig(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, int64_t ts) {
 }  // namespace
 
 bool dist_ready(int ngpu) { return (g_comm || g_loopback) && g_ngpu == ngpu; }
+
+void fuse_exchanges(std::vector<DistStep> &steps, std::vector<moa_pass_desc_t> &passes) {
+    std::vector<DistStep> out;
+    bool synced = false;         // a synchronisation (exchange / barrier) earlier in this exec
+    bool read_since[4] = {};     // buffers read by a pass since the last synchronisation
+    int rename_from = -1, rename_to = -1;
+    auto sync = [&] {
+        synced = true;
+        for (bool &r : read_since) r = false;
+    };
+    for (size_t i = 0; i < steps.size(); i++) {
+        DistStep s = steps[i];
+        if (s.kind == 0 && s.src == rename_from) {
+            s.src = rename_to;
+            passes[s.pass].src = rename_to;
+        }
+        if (s.kind == 1) {
+            if (s.src == rename_from) s.src = rename_to;
+            out.push_back(s);
+            sync();
+            continue;
+        }
+        const bool fusable = s.kind == 0 && i + 1 < steps.size() && steps[i + 1].kind == 1 && steps[i + 1].src == s.dst &&
+                             passes[s.pass].dst == s.dst && !passes[s.pass].ring && passes[s.pass].kind == 0;
+        if (!fusable) {
+            read_since[s.src] = true;
+            out.push_back(s);
+            continue;
+        }
+        const DistStep &x = steps[i + 1];
+        int target;
+        if (!read_since[x.src] && s.src != x.src) {
+            target = x.src;  // later reads of the exchange's destination read here instead
+            rename_from = x.dst;
+            rename_to = x.src;
+        } else if (!read_since[x.dst] && s.src != x.dst) {
+            target = x.dst;
+        } else {
+            out.push_back({3, -1, -1, -1, 0});
+            sync();
+            target = x.dst;
+        }
+        if (!synced) {  // an earlier exec's reads of the target may still be running on a peer
+            out.push_back({3, -1, -1, -1, 0});
+            sync();
+        }
+        out.push_back({2, s.pass, s.src, target, x.count});
+        out.push_back({3, -1, -1, -1, 0});
+        sync();
+        i++;
+    }
+    steps.swap(out);
+}
+
+namespace {
+// Map every rank's scratch buffer `id` into this process (CUDA IPC over
+// NVLink): the handles are all-gathered through the communicator at plan time.
+moa_status_t setup_peers(DistPlan *dp, int id, void *local) {
+    if (!g_nccl.allGather || !g_nccl.allReduce) return fail(MOA_EUNSUPPORTED, "NCCL lacks allGather/allReduce");
+    cudaIpcMemHandle_t h;
+    if (!local || cudaIpcGetMemHandle(&h, local) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOA_EUNSUPPORTED, "cudaIpcGetMemHandle failed");
+    }
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char *d = nullptr;
+    if (cudaMalloc(&d, hb * dp->ngpu) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOA_ENOMEM, "peer handle buffer");
+    }
+    std::vector<char> all(hb * dp->ngpu);
+    cudaStream_t s = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMemcpy(d + hb * dp->rank, &h, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+              g_nccl.allGather(d + hb * dp->rank, d, hb, ncclChar, g_comm, s) == ncclSuccess &&
+              cudaStreamSynchronize(s) == cudaSuccess &&
+              cudaMemcpy(all.data(), d, hb * dp->ngpu, cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (s) cudaStreamDestroy(s);
+    cudaFree(d);
+    if (!ok) {
+        cudaGetLastError();
+        return fail(MOA_ENCCL, "peer handle exchange failed");
+    }
+    for (int g = 0; g < dp->ngpu; g++) {
+        if (g == dp->rank) {
+            dp->peer_buf[id][g] = local;
+            continue;
+        }
+        cudaIpcMemHandle_t ph;
+        std::memcpy(&ph, all.data() + hb * g, hb);
+        if (cudaIpcOpenMemHandle(&dp->peer_buf[id][g], ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MOA_EUNSUPPORTED, "cudaIpcOpenMemHandle failed (no peer access?)");
+        }
+        dp->peer_opened[id][g] = true;
+    }
+    return MOA_OK;
+}
+}  // namespace
+
+moa_status_t dist_finish(DistPlan *dp, void *scratch) {
+    const char *pe = std::getenv("MOA_FFT_PEER");
+    if (pe && pe[0] == '0') return MOA_OK;
+    std::vector<DistStep> steps = dp->steps;
+    std::vector<moa_pass_desc_t> passes = dp->passes;
+    fuse_exchanges(steps, passes);
+    if (!dp->loopback) {  // (the loopback maps the virtual ranks' buffers at exec time)
+        void *local[4] = {nullptr, nullptr, scratch, dp->scratch2};
+        bool need[4] = {};
+        for (auto &s : steps)
+            if (s.kind == 2) need[s.dst] = true;
+        for (int id = 0; id < 4; id++)
+            if (need[id] && (id < 2 || setup_peers(dp, id, local[id]) != MOA_OK))
+                return MOA_OK;  // fused exchanges stay off: the NCCL schedule runs
+        if (cudaMalloc(&dp->barrier_buf, 16) != cudaSuccess) {
+            cudaGetLastError();
+            return MOA_OK;
+        }
+        cudaMemset(dp->barrier_buf, 0, 16);
+    }
+    dp->steps.swap(steps);
+    dp->passes.swap(passes);
+    return MOA_OK;
+}
 
 moa_status_t dist_schedule_1d(int g, int p, int64_t N, moa_dtype_t dtype, std::vector<moa_pass_desc_t> &passes,
                               std::vector<DistStep> &steps, bool lifted_order) {
@@ -237,6 +365,10 @@ moa_status_t dist_plan_3d(DistPlan *&dp, int64_t n0, int64_t n1, int64_t n2, moa
 
 void dist_plan_free(DistPlan *dp) {
     if (!dp) return;
+    for (int id = 0; id < 4; id++)
+        for (int g = 0; g < 8; g++)
+            if (dp->peer_opened[id][g]) cudaIpcCloseMemHandle(dp->peer_buf[id][g]);
+    if (dp->barrier_buf) cudaFree(dp->barrier_buf);
     if (dp->scratch2) cudaFree(dp->scratch2);
     delete dp;
 }
@@ -244,7 +376,7 @@ void dist_plan_free(DistPlan *dp) {
 int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes) {
     (void)passes;
     int c = 0;
-    for (auto &s : dp->steps) c += s.kind == 0;
+    for (auto &s : dp->steps) c += s.kind == 0 || s.kind == 2;
     return c;
 }
 
@@ -257,11 +389,20 @@ moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes,
     for (size_t i = 0; i < dp->steps.size(); i++) {
         const DistStep &st = dp->steps[i];
         if (evs) cudaEventRecord(evs[i], s);
-        if (st.kind == 0) {
+        if (st.kind == 0 || st.kind == 2) {
             const moa_pass_desc_t &d = passes[st.pass];
-            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[d.dst], tabs[st.pass], s,
-                                        pass_mods(flags, size_t(st.pass), passes.size(), N));
+            PassMods mods = pass_mods(flags, size_t(st.pass), passes.size(), N);
+            if (st.kind == 2) {  // the exchange folded into the stores: NVLink writes into every rank's scratch2
+                mods.npeers = dp->ngpu;
+                for (int g = 0; g < dp->ngpu; g++) mods.peers[g] = dp->peer_buf[st.dst][g];
+                mods.log_chunk = log2_exact(st.count);
+                mods.self_off = int64_t(dp->rank) * st.count;
+            }
+            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[st.kind == 2 ? st.dst : d.dst], tabs[st.pass], s, mods);
             if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("dist pass: ") + cudaGetErrorString(e));
+        } else if (st.kind == 3) {  // every rank's fused stores have landed before anyone reads them
+            ncclResult_t r = g_nccl.allReduce(dp->barrier_buf, dp->barrier_buf, 1, ncclFloat, ncclSum, g_comm, s);
+            if (r != ncclSuccess) return nccl_fail(r, "barrier");
         } else {
             const size_t cnt = size_t(st.count) * 2;
             ncclResult_t r = g_nccl.alltoAll(bufs[st.src], bufs[st.dst], cnt, dtype == MOA_C128 ? ncclDouble : ncclFloat,
@@ -355,11 +496,13 @@ moa_status_t moa_dist_describe(int rank, int ngpu, int is3d, int64_t n0, int64_t
         st = dist_schedule_1d(rank, ngpu, n0, dtype, ps, ss, (flags & MOA_FFT_LIFTED_ORDER) != 0);
     }
     if (st) return st;
+    const char *pe = std::getenv("MOA_FFT_PEER");
+    if (!(pe && pe[0] == '0')) fuse_exchanges(ss, ps);  // what a plan executes when peer mapping succeeds
     if (int(ps.size()) > max_passes || int(ss.size()) > max_steps) return fail(MOA_EINVAL, "dist_describe: arrays too small");
     for (size_t i = 0; i < ps.size(); i++) passes[i] = ps[i];
     for (size_t i = 0; i < ss.size(); i++) {
         kinds[i] = ss[i].kind;
-        srcs[i] = ss[i].kind == 0 ? ss[i].pass : ss[i].src;
+        srcs[i] = (ss[i].kind == 0 || ss[i].kind == 2) ? ss[i].pass : ss[i].src;
         dsts[i] = ss[i].dst;
         counts[i] = ss[i].count;
     }

@@ -18,7 +18,9 @@ namespace moa {
 // complex elements per peer from buffer src to buffer dst (ids as in
 // moa_pass_desc_t: 0 in, 1 out, 2 scratch, 3 scratch2).
 struct DistStep {
-    int kind;  // 0 = pass (index into passes), 1 = all-to-all
+    int kind;  // 0 = pass (index into passes), 1 = all-to-all, 2 = pass fused with the
+               // all-to-all that followed it (stores to the peers' buffer `dst`, `count`
+               // elements per peer), 3 = barrier (every rank's previous steps are done)
     int pass;
     int src, dst;
     int64_t count;
@@ -32,7 +34,23 @@ struct DistPlan {
     int64_t local_elems = 0;
     size_t esize = 16;
     void *scratch2 = nullptr;
+    // fused exchanges (kind 2): every rank's scratch buffers (ids 2, 3), mapped
+    // into this process over NVLink (CUDA IPC); peer_opened marks handles to close
+    void *peer_buf[4][8] = {};
+    bool peer_opened[4][8] = {};
+    void *barrier_buf = nullptr;
 };
+
+// Fold every all-to-all that directly follows a pass writing its source buffer
+// into that pass's stores (kind 2) plus a barrier (kind 3).  The fused stores go
+// to a buffer no rank can still be reading: the exchange's source buffer when
+// nothing read it since the last synchronisation (later reads of the exchange's
+// destination are renamed to it), else its destination; a barrier is inserted
+// first when there was no synchronisation yet in the exec.  Host only.
+void fuse_exchanges(std::vector<DistStep> &steps, std::vector<moa_pass_desc_t> &passes);
+// After the plan's scratch (buffer 2) exists: map the peers' buffers and fuse
+// the exchanges (default; MOA_FFT_PEER=0 keeps every all-to-all in NCCL).
+moa_status_t dist_finish(DistPlan *dp, void *scratch);
 
 bool dist_ready(int ngpu);
 moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype, bool lifted_order = false);

@@ -138,6 +138,10 @@ struct KArgs {
     int32_t discard;  // ring == 1: discard the consumed ring lines (no write-back)
     int32_t conj_in, conj_out;  // inverse transform: conjugate loads / results (PassMods)
     double scale;               // results times scale (1: none)
+    int32_t npeers;             // fused exchange: stores go to peers[q >> log_chunk] (PassMods)
+    int32_t log_chunk;
+    int64_t self_off;
+    void *peers[8];
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -355,6 +359,17 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     }
 
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
+    if (a.npeers) {  // fused all-to-all: send-layout offset q -> peer q / chunk (NVLink store)
+        const uint64_t pol = l2_policy(false);
+        const int64_t cmask = (int64_t(1) << a.log_chunk) - 1;
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+            const int64_t q = oo + (a.ksplit >= LR ? int64_t(tB + m * TPL) * a.out_kstr : kaddr(a, tB + m * TPL));
+            V *dst = reinterpret_cast<V *>(a.peers[q >> a.log_chunk]) + a.self_off + (q & cmask);
+            st_pol(dst, pts[m], pol);
+        }
+        return;
+    }
     {
         const uint64_t pol = l2_policy(a.ring == 2);
         if (a.ksplit >= LR) {  // the common case: one affine stride per point
@@ -626,6 +641,10 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.conj_in = mods.conj_in;
     a.conj_out = mods.conj_out;
     a.scale = mods.scale;
+    a.npeers = mods.npeers;
+    a.log_chunk = mods.log_chunk;
+    a.self_off = mods.self_off;
+    for (int i = 0; i < 8; i++) a.peers[i] = mods.peers[i];
     a.in = in;
     a.out = out;
     a.ndig = d.ndig;

@@ -57,6 +57,14 @@ struct PassMods {
     int conj_in = 0;
     int conj_out = 0;
     double scale = 1.0;
+    // Fused exchange (processor-level lifting): the pass stores straight into
+    // the peers' buffers -- the all-to-all that followed it is folded into its
+    // store.  Send-layout offset q goes to peers[q >> log_chunk] at
+    // self_off + (q & (chunk - 1)).  npeers == 0: an ordinary local store.
+    int npeers = 0;
+    void *peers[8] = {};
+    int log_chunk = 0;
+    int64_t self_off = 0;
 };
 // the modifiers of pass i of npass under `flags` (MOA_FFT_INVERSE / _NORMALIZE)
 PassMods pass_mods(uint32_t flags, size_t i, size_t npass, int64_t N);

@@ -102,6 +102,20 @@ def run_dist(schedules, shards):
             for r in range(p):
                 d = schedules[r]["passes"][schedules[r]["steps"][i][1]]
                 run_pass(d, bufs[r][d["src"]], bufs[r][d["dst"]])
+        elif st[0] == "barrier":
+            continue
+        elif st[0] == "fused":
+            # the pass's stores, in its send layout, land in rank h's buffer t at g c
+            _, _, t, c = st
+            sends = []
+            for r in range(p):
+                d = schedules[r]["passes"][schedules[r]["steps"][i][1]]
+                send = np.full(m, np.nan + 0j)
+                run_pass(d, bufs[r][d["src"]], send)
+                sends.append(send)
+            for h in range(p):
+                for g in range(p):
+                    bufs[h][t][g * c:(g + 1) * c] = sends[g][h * c:(h + 1) * c]
         else:
             _, s, t, c = st
             snap = [bufs[g][s].copy() for g in range(p)]

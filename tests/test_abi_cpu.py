@@ -147,29 +147,44 @@ def test_psi_3d_descriptors(monkeypatch):
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
 
 
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("p", [2, 4, 8])
-def test_dist_1d_schedule_host_simulation(p):
-    # processor-level lifting: every rank's ONF + the all-to-all chunk maps reproduce the DFT
+def test_dist_1d_schedule_host_simulation(monkeypatch, p, peer):
+    # processor-level lifting: every rank's ONF + the all-to-all chunk maps reproduce
+    # the DFT -- with every exchange in NCCL (peer 0), or with E2 and E3 fused into
+    # the stores of the pass before them (NVLink peer stores) and E1 left in NCCL
+    monkeypatch.setenv("MOA_FFT_PEER", peer)
     N = 1 << 12
     x = synth.fill(N, 8, synth.UNIFORM)
     sch = [m.moa_dist_describe(r, p, N, "c64") for r in range(p)]
     kinds = [s[0] for s in sch[0]["steps"]]
-    assert kinds.count("alltoall") == 3
+    if peer == "0":
+        assert kinds.count("alltoall") == 3
+    else:
+        assert kinds.count("alltoall") == 1 and kinds.count("fused") == 2
+        # a fused pass never stores into a buffer it (or any pass since the last
+        # synchronisation) reads
+        for i, s in enumerate(sch[0]["steps"]):
+            if s[0] == "fused":
+                assert sch[0]["passes"][s[1]]["src"] != s[2]
+                assert sch[0]["steps"][i + 1][0] == "barrier"
     outs = run_dist(sch, np.split(x, p))
     ref = oracle.fft_radix2(x)
     got = np.concatenate(outs)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
 
 
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("p", [2, 4, 8])
-def test_dist_1d_lifted_order_schedule(p):
+def test_dist_1d_lifted_order_schedule(monkeypatch, p, peer):
     # MOA_FFT_LIFTED_ORDER: no third all-to-all, no unpack; rank g holds X[g + p k2]
     # at offset k2 -- the final transpose is never executed
     N = 1 << 12
     x = synth.fill(N, 9, synth.UNIFORM)
+    monkeypatch.setenv("MOA_FFT_PEER", peer)
     sch = [m.moa_dist_describe(r, p, N, "c128", flags=m.MOA_FFT_LIFTED_ORDER) for r in range(p)]
     kinds = [s[0] for s in sch[0]["steps"]]
-    assert kinds.count("alltoall") == 2
+    assert kinds.count("alltoall") + kinds.count("fused") == 2
     outs = run_dist(sch, np.split(x, p))
     ref = oracle.fft_radix2(x)
     for g in range(p):
@@ -177,12 +192,17 @@ def test_dist_1d_lifted_order_schedule(p):
         assert np.linalg.norm(outs[g] - want) / np.linalg.norm(want) < 1e-12
 
 
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("p", [2, 4, 8])
-def test_dist_3d_schedule_host_simulation(p):
+def test_dist_3d_schedule_host_simulation(monkeypatch, p, peer):
+    monkeypatch.setenv("MOA_FFT_PEER", peer)
     shape = (16, 8, 4)
     x = synth.fill(int(np.prod(shape)), 9, synth.NORMAL).reshape(shape)
     sch = [m.moa_dist_describe(r, p, shape, "c128") for r in range(p)]
-    assert [s[0] for s in sch[0]["steps"]].count("alltoall") == 1
+    kinds = [s[0] for s in sch[0]["steps"]]
+    assert kinds.count("alltoall") + kinds.count("fused") == 1
+    if peer == "1":      # no synchronisation earlier in the exec: a barrier precedes the fused y-pass
+        assert kinds[kinds.index("fused") - 1] == "barrier"
     shards = [np.ascontiguousarray(s).reshape(-1) for s in np.split(x, p, axis=0)]
     outs = run_dist(sch, shards)
     ref = oracle.fft3d(x)

@@ -59,6 +59,13 @@ def _worker(rank, world, port, kind, q):
             if st[0] == "pass":
                 d = sch["passes"][st[1]]
                 run_pass(d, bufs[d["src"]], bufs[d["dst"]])
+            elif st[0] == "barrier":
+                dist.barrier()
+            elif st[0] == "fused":                              # pass + all-to-all by its stores
+                d = sch["passes"][st[1]]
+                send = np.zeros(L, np.complex128)
+                run_pass(d, bufs[d["src"]], send)
+                bufs[st[2]] = _alltoall(send, st[3], world)
             else:
                 _, s, t, c = st
                 bufs[t] = _alltoall(bufs[s], c, world)

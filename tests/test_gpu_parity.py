@@ -193,9 +193,13 @@ def test_3d(m, torch_cuda, monkeypatch, shape, dtype, fuse, rot):
 
 
 # ---------------------------------------------------------------- loopback processor lifting
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("p", [2, 4, 8])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_dist_1d_loopback(m, torch_cuda, p, dtype):
+def test_dist_1d_loopback(m, torch_cuda, monkeypatch, p, dtype, peer):
+    # peer 1: E2 and E3 fused into the stores of pass A / the last local pass
+    # (every virtual rank's kernel writes straight into the others' buffers)
+    monkeypatch.setenv("MOA_FFT_PEER", peer)
     torch = torch_cuda
     N = 1 << 20
     x = synth.fill(N, 3, synth.UNIFORM, dtype)
@@ -213,8 +217,10 @@ def test_dist_1d_loopback(m, torch_cuda, p, dtype):
     assert rel_l2(y, ref) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("p", [2, 4, 8])
-def test_dist_3d_loopback(m, torch_cuda, p):
+def test_dist_3d_loopback(m, torch_cuda, monkeypatch, p, peer):
+    monkeypatch.setenv("MOA_FFT_PEER", peer)
     torch = torch_cuda
     shape = (64, 32, 16)
     x = synth.fill(int(np.prod(shape)), 4, synth.NORMAL).reshape(shape)
