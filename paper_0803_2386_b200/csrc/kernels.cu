@@ -133,6 +133,7 @@ struct KArgs {
     int64_t out_kstr_hi;
     int32_t nodft;  // moa_pass_desc_t kind == 1
     int32_t W, LS;   // lines per tile, smem line stride (elements)
+    int32_t lW;      // log2(W)
     int32_t lf_load, lf_store;
     int32_t ring;     // 0: HBM both sides; 1: loads from the L2 ring; 2: stores to the ring
     int32_t discard;  // ring == 1: discard the consumed ring lines (no write-back)
@@ -269,10 +270,10 @@ struct TileMap {
 template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
     const int tid = threadIdx.x;
     TileMap m;
-    m.lA = a.lf_load ? tid % a.W : tid / TPL;
-    m.tA = a.lf_load ? tid / a.W : tid % TPL;
-    m.lB = a.lf_store ? tid % a.W : tid / TPL;
-    m.tB = a.lf_store ? tid / a.W : tid % TPL;
+    m.lA = a.lf_load ? tid & (a.W - 1) : tid / TPL;
+    m.tA = a.lf_load ? tid >> a.lW : tid % TPL;
+    m.lB = a.lf_store ? tid & (a.W - 1) : tid / TPL;
+    m.tB = a.lf_store ? tid >> a.lW : tid % TPL;
     return m;
 }
 
@@ -282,7 +283,9 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
 // pair_kernel); the ring side's address gets slot * ringG added.
 template <typename V, int LR>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
-                                             V (&pts)[1 << (LR < 4 ? LR : 4)]) {
+                                             V (&pts)[1 << (LR < 4 ? LR : 4)], int64_t b_io, int64_t b_oo,
+                                             int64_t b_te) {
+    (void)line0;
     constexpr int LP = LR < 4 ? LR : 4;
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
@@ -319,9 +322,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     if (a.ring == 1 && a.discard) {
         __syncthreads();
         constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
-        int64_t io, u0, u1;
-        line_offsets(a, line0 + lA, io, u0, u1);
-        io += ring_off;
+        const int64_t io = b_io + int64_t(lA) * a.in_str[0] + ring_off;
         const V *in = reinterpret_cast<const V *>(a.in);
 #pragma unroll
         for (int m = 0; m < P; m++) {
@@ -334,8 +335,9 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     // ---- 3. lifted weights w_N^{(e k) mod N} for k = tB + m R/P: one two-level
     //         lookup for k = tB, one for the increment, then a multiplicative chain
     //         in double precision (<= 15 products, ~1e-15 relative)
-    int64_t oo, te, u0;
-    line_offsets(a, line0 + lB, u0, oo, te);
+    // (the W lines of a tile share every digit but digit 0, which W divides)
+    int64_t oo = b_oo + int64_t(lB) * a.out_str[0];
+    const int64_t te = b_te + int64_t(lB) * a.tw_str[0];
     if (a.ring == 2) oo += ring_off;
     if (a.twmask) {
         const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
@@ -390,8 +392,9 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     constexpr int LP = LR < 4 ? LR : 4;
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     const TileMap mp = tile_map<TPL>(a);
-    int64_t io, u0, u1;
-    line_offsets(a, line0 + mp.lA, io, u0, u1);
+    int64_t b_io, b_oo, b_te;
+    line_offsets(a, line0, b_io, b_oo, b_te);  // the tile's first line; line l adds l * str[0]
+    int64_t io = b_io + int64_t(mp.lA) * a.in_str[0];
     if (a.ring == 1) io += ring_off;
     V pts[P];
     // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
@@ -406,7 +409,7 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
 #pragma unroll
         for (int m = 0; m < P; m++) pts[m].y = -pts[m].y;
     }
-    tile_compute<V, LR>(a, line0, sm, ring_off, pts);
+    tile_compute<V, LR>(a, line0, sm, ring_off, pts, b_io, b_oo, b_te);
 }
 
 template <typename V, int LR>
@@ -670,6 +673,7 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.out_kstr_hi = d.out_kstr_hi;
     a.nodft = d.kind == 1;
     a.W = d.W;
+    a.lW = log2_exact(d.W);
     a.LS = (1 << d.logR) + d.line_pad;
     a.lf_load = d.lf_load;
     a.lf_store = d.lf_store;
