@@ -15,8 +15,8 @@
 //                self-sorting (autosort) schedule.  The paper's input bit reversal
 //                P_n is never materialised: each step's output index map
 //                absorbs it (step a3).  Exchanges between steps go through
-//                XOR-swizzled shared memory (conflict-free for the access
-//                patterns used; see psi_choose_tile for the line padding).
+//                shared memory with one pad element per 16 and a line stride
+//                chosen on the host by a bank-conflict model (psi_choose_tile).
 //   3. twiddle -- the lifted weights w_N^{(j k) mod N} from a
 //                two-level table (exact integer exponent; two table reads and one
 //                complex multiply), fused before the store.
