@@ -47,9 +47,28 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 cmul(float2 a, float2 w) {
     return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
 }
+// Paired complex64 lines: two ADJACENT lines of a line-coalesced complex64
+// pass in one 16-byte quad (re0, im0, re1, im1) -- one 128-bit load / store /
+// exchange per two points and one set of step twiddles and address
+// arithmetic for both lines (the complex64 passes are issue-bound).
+__device__ __forceinline__ float4 cadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 csub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
+__device__ __forceinline__ float4 cmul(float4 a, float2 w) {
+    return make_float4(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x), fmaf(a.z, w.x, -a.w * w.y),
+                       fmaf(a.z, w.y, a.w * w.x));
+}
+__device__ __forceinline__ float4 cmul(float4 a, float4 w) {  // a different weight per line
+    return make_float4(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x), fmaf(a.z, w.z, -a.w * w.w),
+                       fmaf(a.z, w.w, a.w * w.z));
+}
 template <typename V> struct RealOf;
 template <> struct RealOf<double2> { using type = double; };
 template <> struct RealOf<float2> { using type = float; };
+template <> struct RealOf<float4> { using type = float; };
+// element (one complex) and step-twiddle type of a pass value type
+template <typename V> struct ElemOf { using type = V; };
+template <> struct ElemOf<float4> { using type = float2; };
+template <typename V> __host__ __device__ constexpr int lines_per_lane() { return std::is_same<V, float4>::value ? 2 : 1; }
 template <typename V> __device__ __forceinline__ V mk(typename RealOf<V>::type x, typename RealOf<V>::type y) {
     V v;
     v.x = x;
@@ -62,7 +81,10 @@ template <typename V> __device__ __forceinline__ V mk(typename RealOf<V>::type x
 template <int E, typename V> __device__ __forceinline__ V rot16(V z) {
     using T = typename RealOf<V>::type;
     constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173, H = 0.70710678118654752440;
-    if constexpr (E == 0) return z;
+    if constexpr (std::is_same<V, float4>::value) {  // both lines of a pair
+        const float2 lo = rot16<E>(make_float2(z.x, z.y)), hi = rot16<E>(make_float2(z.z, z.w));
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+    } else if constexpr (E == 0) return z;
     else if constexpr (E == 4) return mk<V>(z.y, -z.x);                          // * (-i)
     else if constexpr (E == 2) return mk<V>((z.x + z.y) * T(H), (z.y - z.x) * T(H));   // * (1-i)/sqrt2
     else if constexpr (E == 6) return mk<V>((z.y - z.x) * T(H), -(z.x + z.y) * T(H));  // * (-1-i)/sqrt2
@@ -185,6 +207,17 @@ __device__ __forceinline__ float2 ld_pol(const float2 *p, uint64_t pol) {
     asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ float4 ld_pol(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_pol(float4 *p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void st_pol(double2 *p, double2 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
@@ -198,7 +231,8 @@ __device__ __forceinline__ void st_pol(float2 *p, float2 v, uint64_t pol) {
 // j + r R/Q, multiplies by w_{NS Q}^{(j mod NS) r}, transforms, and writes to
 // (j / NS) NS Q + (j mod NS) + r NS (the self-sorting index map).
 template <int LR, int LP, int LQ, int LNS, bool LAST, int LB, typename V>
-__device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int t, const V *__restrict__ twR) {
+__device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int t,
+                                              const typename ElemOf<V>::type *__restrict__ twR) {
     constexpr int R = 1 << LR, P = 1 << LP, Q = 1 << LQ, NS = 1 << LNS, G = P / Q;
 #pragma unroll
     for (int u = 0; u < G; u++) {
@@ -231,7 +265,7 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
 // for free there and no extra transposition is needed for a strided side.
 template <int LR, int LP, int LB, int S, int NSTEP, typename V>
 __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int lA, int tA, int lB, int tB,
-                                         const V *__restrict__ twR) {
+                                         const typename ElemOf<V>::type *__restrict__ twR) {
     // radix P for every step but the last, which takes the remainder (so step 0,
     // whose writes are strided by its radix, always has radix 16)
     constexpr int LQL = LR - LP * (NSTEP - 1);
@@ -253,6 +287,7 @@ __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int l
 
 __device__ __forceinline__ double2 cvt_tw(double2 w, double2) { return w; }
 __device__ __forceinline__ float2 cvt_tw(double2 w, float2) { return make_float2(float(w.x), float(w.y)); }
+__device__ __forceinline__ float2 cvt_tw(double2 w, float4) { return make_float2(float(w.x), float(w.y)); }
 
 // w_N^e from the two-level double-precision table (exact integer exponent)
 __device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, const double2 *__restrict__ lo, int64_t e,
@@ -290,8 +325,10 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
     constexpr int NSTEP = LR == 0 ? 1 : (LR + LP - 1) / LP;
-    V *__restrict__ out = reinterpret_cast<V *>(a.out);
-    const V *__restrict__ twR = reinterpret_cast<const V *>(a.twR);
+    using E = typename ElemOf<V>::type;
+    constexpr int LPL = lines_per_lane<V>();  // lines per lane (2: paired complex64)
+    E *__restrict__ out = reinterpret_cast<E *>(a.out);
+    const E *__restrict__ twR = reinterpret_cast<const E *>(a.twR);
     const TileMap mp = tile_map<TPL>(a);
     const int lA = mp.lA, tA = mp.tA, lB = mp.lB, tB = mp.tB;
 
@@ -319,14 +356,14 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     // ---- ring: every thread has consumed its loads (the exchanges above, or the
     //      barrier here); drop the ring lines this tile read from L2 without a
     //      write-back (discard.global.L2): the intermediate never reaches HBM
-    if (a.ring == 1 && a.discard) {
+    if (LPL == 1 && a.ring == 1 && a.discard) {
         __syncthreads();
         constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
         const int64_t io = b_io + int64_t(lA) * a.in_str[0] + ring_off;
-        const V *in = reinterpret_cast<const V *>(a.in);
+        const E *in = reinterpret_cast<const E *>(a.in);
 #pragma unroll
         for (int m = 0; m < P; m++) {
-            const V *p = in + io + int64_t(tA + m * TPL) * a.in_kstr;
+            const E *p = in + io + int64_t(tA + m * TPL) * a.in_kstr;
             if ((reinterpret_cast<uintptr_t>(p) & 127) == 0 && (a.in_kstr != 1 || ((tA + m * TPL) % EPL) == 0))
                 asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
         }
@@ -336,8 +373,8 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     //         lookup for k = tB, one for the increment, then a multiplicative chain
     //         in double precision (<= 15 products, ~1e-15 relative)
     // (the W lines of a tile share every digit but digit 0, which W divides)
-    int64_t oo = b_oo + int64_t(lB) * a.out_str[0];
-    const int64_t te = b_te + int64_t(lB) * a.tw_str[0];
+    int64_t oo = b_oo + int64_t(LPL * lB) * a.out_str[0];
+    const int64_t te = b_te + int64_t(LPL * lB) * a.tw_str[0];
     if (a.ring == 2) oo += ring_off;
     if (a.twmask) {
         const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
@@ -345,10 +382,24 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         const int64_t e0 = te + a.tw_off;
         double2 w = tw_lookup(hi, lo, (e0 * tB) & a.twmask, a.twh);
         const double2 ws = tw_lookup(hi, lo, (e0 * TPL) & a.twmask, a.twh);
+        if constexpr (LPL == 1) {
 #pragma unroll
-        for (int m = 0; m < P; m++) {
-            pts[m] = cmul(pts[m], cvt_tw(w, V{}));
-            if (m + 1 < P) w = cmul(w, ws);
+            for (int m = 0; m < P; m++) {
+                pts[m] = cmul(pts[m], cvt_tw(w, V{}));
+                if (m + 1 < P) w = cmul(w, ws);
+            }
+        } else {  // the pair's second line has its own exponent base
+            const int64_t e1 = e0 + a.tw_str[0];
+            double2 w1 = tw_lookup(hi, lo, (e1 * tB) & a.twmask, a.twh);
+            const double2 ws1 = tw_lookup(hi, lo, (e1 * TPL) & a.twmask, a.twh);
+#pragma unroll
+            for (int m = 0; m < P; m++) {
+                pts[m] = cmul(pts[m], make_float4(float(w.x), float(w.y), float(w1.x), float(w1.y)));
+                if (m + 1 < P) {
+                    w = cmul(w, ws);
+                    w1 = cmul(w1, ws1);
+                }
+            }
         }
     }
 
@@ -357,7 +408,10 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         using T = typename RealOf<V>::type;
         const T sr = T(a.scale), si = a.conj_out ? -T(a.scale) : T(a.scale);
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = mk<V>(pts[m].x * sr, pts[m].y * si);
+        for (int m = 0; m < P; m++) {
+            if constexpr (LPL == 1) pts[m] = mk<V>(pts[m].x * sr, pts[m].y * si);
+            else pts[m] = make_float4(pts[m].x * sr, pts[m].y * si, pts[m].z * sr, pts[m].w * si);
+        }
     }
 
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
@@ -367,21 +421,21 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
 #pragma unroll
         for (int m = 0; m < P; m++) {
             const int64_t q = oo + (a.ksplit >= LR ? int64_t(tB + m * TPL) * a.out_kstr : kaddr(a, tB + m * TPL));
-            V *dst = reinterpret_cast<V *>(a.peers[q >> a.log_chunk]) + a.self_off + (q & cmask);
-            st_pol(dst, pts[m], pol);
+            E *dst = reinterpret_cast<E *>(a.peers[q >> a.log_chunk]) + a.self_off + (q & cmask);
+            st_pol(reinterpret_cast<V *>(dst), pts[m], pol);
         }
         return;
     }
     {
         const uint64_t pol = l2_policy(a.ring == 2);
         if (a.ksplit >= LR) {  // the common case: one affine stride per point
-            V *base = out + oo + int64_t(tB) * a.out_kstr;
+            E *base = out + oo + int64_t(tB) * a.out_kstr;
             const int64_t step = int64_t(TPL) * a.out_kstr;
 #pragma unroll
-            for (int m = 0; m < P; m++) st_pol(base + m * step, pts[m], pol);
+            for (int m = 0; m < P; m++) st_pol(reinterpret_cast<V *>(base + m * step), pts[m], pol);
         } else {
 #pragma unroll
-            for (int m = 0; m < P; m++) st_pol(out + oo + kaddr(a, tB + m * TPL), pts[m], pol);
+            for (int m = 0; m < P; m++) st_pol(reinterpret_cast<V *>(out + oo + kaddr(a, tB + m * TPL)), pts[m], pol);
         }
     }
 }
@@ -391,23 +445,28 @@ template <typename V, int LR>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
     constexpr int LP = LR < 4 ? LR : 4;
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
+    using E = typename ElemOf<V>::type;
+    constexpr int LPL = lines_per_lane<V>();
     const TileMap mp = tile_map<TPL>(a);
     int64_t b_io, b_oo, b_te;
     line_offsets(a, line0, b_io, b_oo, b_te);  // the tile's first line; line l adds l * str[0]
-    int64_t io = b_io + int64_t(mp.lA) * a.in_str[0];
+    int64_t io = b_io + int64_t(LPL * mp.lA) * a.in_str[0];
     if (a.ring == 1) io += ring_off;
     V pts[P];
     // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
     {
         const uint64_t pol = l2_policy(a.ring == 1);
-        const V *base = reinterpret_cast<const V *>(a.in) + io + int64_t(mp.tA) * a.in_kstr;
+        const E *base = reinterpret_cast<const E *>(a.in) + io + int64_t(mp.tA) * a.in_kstr;
         const int64_t step = int64_t(TPL) * a.in_kstr;
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = ld_pol(base + m * step, pol);
+        for (int m = 0; m < P; m++) pts[m] = ld_pol(reinterpret_cast<const V *>(base + m * step), pol);
     }
     if (a.conj_in) {  // inverse transform: DFT of conj(x) (the plan's first pass)
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m].y = -pts[m].y;
+        for (int m = 0; m < P; m++) {
+            pts[m].y = -pts[m].y;
+            if constexpr (LPL == 2) pts[m].w = -pts[m].w;
+        }
     }
     tile_compute<V, LR>(a, line0, sm, ring_off, pts, b_io, b_oo, b_te);
 }
@@ -415,7 +474,7 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
 template <typename V, int LR>
 __global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<V *>(smem_raw), 0);
+    tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }
 
 // A fused pass pair: pass A writes its output to an L2-resident ring of
@@ -636,6 +695,8 @@ template <typename V, int... Is> constexpr auto make_pair_table(std::integer_seq
 const std::array<PFn<double2>, 36> kPair128 = make_pair_table<double2>(std::make_integer_sequence<int, 36>{});
 const std::array<PFn<float2>, 36> kPair64 = make_pair_table<float2>(std::make_integer_sequence<int, 36>{});
 const std::array<KFn<double2>, 13> kTab128 = make_table<double2>(std::make_integer_sequence<int, 13>{});
+// paired complex64 lines (float4 = two adjacent lines)
+const std::array<KFn<float4>, 13> kTabPair64 = make_table<float4>(std::make_integer_sequence<int, 13>{});
 const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
 
 KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines,
@@ -688,6 +749,27 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     int64_t nlines = 0;
     KArgs a = fill_args(d, in, out, tb, &nlines, mods);
     const int64_t tiles = nlines / d.W;
+    // complex64 passes of >= 2^10-point lines coalesced along the lines on both
+    // sides (digit 0 unit stride in and out, even tile width): two adjacent
+    // lines per lane -- half the threads and memory instructions per tile
+    // (measured: 3-D c64 y-pass 5.12 -> 4.04 ms; slower for <= 2^8-point lines)
+    if constexpr (std::is_same<V, float2>::value) {
+        const char *pe = std::getenv("MOA_FFT_C64PAIR");
+        const int min_lr = pe && pe[0] == '1' ? 4 : 10;
+        if (!(pe && pe[0] == '0') && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
+            d.in_str[0] == 1 && d.out_str[0] == 1 && d.W >= 2 && d.logR >= min_lr && d.out_ksplit >= d.logR) {
+            KArgs b = a;
+            b.W = d.W / 2;
+            b.lW = log2_exact(b.W);
+            KFn<float4> f = kTabPair64[d.logR];
+            if (d.smem_bytes > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
+                if (e != cudaSuccess) return e;
+            }
+            f<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads / 2)), size_t(d.smem_bytes), stream>>>(b);
+            return cudaGetLastError();
+        }
+    }
     KFn<V> fn = tab[d.logR];
     if (d.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
