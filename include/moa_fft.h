@@ -267,6 +267,17 @@ moa_status_t moa_psi_describe_3d(int64_t n0, int64_t n1, int64_t n2, moa_dtype_t
 /* The planner's lifting for (n, batch, dtype) on one GPU. */
 moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64_t *radices, int max_rad,
                               int *nrad);
+/*
+ * moa_pass_move -- test hook: execute ONE pass descriptor as a
+ * pure data movement on the GPU -- kind forced to 1 (no DFT), no twiddle, no
+ * ring -- so that out[store(line, k)] = in[load(line, k)] for every line and
+ * point of the ONF, through exactly the address arithmetic, thread mappings
+ * and shared-memory exchanges the pass uses.  Lets tests compare the kernels'
+ * movement bit-exactly with the descriptor's index maps on integer payloads.
+ * Stream-ordered; d must come from moa_psi_describe* / moa_fft_plan_describe.
+ */
+moa_status_t moa_pass_move(const moa_pass_desc_t *d, moa_dtype_t dtype, const void *in, void *out, void *stream);
+
 /* The descriptors a plan actually executes. */
 moa_status_t moa_fft_plan_describe(moa_fft_plan_t plan, moa_pass_desc_t *out, int max_passes, int *npasses);
 

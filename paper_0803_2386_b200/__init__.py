@@ -28,7 +28,7 @@ EXPORTS = [
     "moa_fft_get_unique_id", "moa_fft_dist_init", "moa_fft_dist_finalize", "moa_fft_dist_loopback",
     "moa_fft_exec_loopback", "moa_dist_describe", "moa_psi_describe", "moa_psi_describe_3d",
     "moa_plan_radices", "moa_fft_plan_describe", "moa_fft_prof_begin", "moa_fft_prof_end",
-    "moa_fft_plan_ex", "moa_fft_plan_3d_ex", "moa_fft_output_index",
+    "moa_fft_plan_ex", "moa_fft_plan_3d_ex", "moa_fft_output_index", "moa_pass_move",
 ]
 
 
@@ -48,6 +48,18 @@ class PassDesc(ctypes.Structure):
         ("ring", ctypes.c_int32), ("ring_slots", ctypes.c_int32), ("ring_lag", ctypes.c_int32),
         ("ring_discard", ctypes.c_int32), ("ring_groups", ctypes.c_int64), ("ring_G", ctypes.c_int64),
     ]
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "PassDesc":
+        s = cls()
+        for name, _ in cls._fields_:
+            if name in ("ext", "in_str", "out_str", "tw_str"):
+                arr = getattr(s, name)
+                for i, v in enumerate(d[name]):
+                    arr[i] = v
+            elif name in d:
+                setattr(s, name, d[name])
+        return s
 
     def to_dict(self) -> dict:
         nd = self.ndig
@@ -82,6 +94,7 @@ def _load():
         "moa_fft_plan_ex": [P(vp), i64, i64, i32, i32, ctypes.c_uint32],
         "moa_fft_plan_3d_ex": [P(vp), i64, i64, i64, i32, i32, ctypes.c_uint32],
         "moa_fft_output_index": [vp, P(i64), i64],
+        "moa_pass_move": [P(PassDesc), i32, vp, vp, vp],
         "moa_fft_exec": [vp, vp, vp, vp],
         "moa_fft_exec_host": [vp, vp, vp, vp],
         "moa_fft_destroy": [vp],
@@ -156,6 +169,13 @@ def moa_fft_output_index(plan: int, n: int):
     pos = np.empty(n, dtype=np.int64)
     _check(lib.moa_fft_output_index(plan, pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n))
     return pos
+
+
+def moa_pass_move(desc: dict, dtype, in_ptr: int, out_ptr: int, stream: int = 0) -> None:
+    """Test hook: run one pass descriptor (a dict from moa_psi_describe*) as a
+    pure data movement on the GPU (see include/moa_fft.h)."""
+    d = PassDesc.from_dict(desc)
+    _check(lib.moa_pass_move(ctypes.byref(d), _dt(dtype), in_ptr, out_ptr, stream))
 
 
 def moa_fft_plan_lift(n: int, batch: int, dtype, radices) -> int:

@@ -643,6 +643,21 @@ moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64
     return MOA_OK;
 }
 
+moa_status_t moa_pass_move(const moa_pass_desc_t *d, moa_dtype_t dtype, const void *in, void *out, void *stream) {
+    if (!d || !in || !out) return fail(MOA_EINVAL, "pass_move: null argument");
+    if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "pass_move: unknown dtype");
+    if (d->kind > 1 || d->logR < 0 || d->logR > 12 || d->ndig < 0 || d->ndig > MOA_MAX_DIGITS)
+        return fail(MOA_EINVAL, "pass_move: not a lifted-pass descriptor");
+    moa_pass_desc_t m = *d;
+    m.kind = 1;
+    m.twN = 1;
+    m.ring = 0;
+    DevTables none;
+    cudaError_t e = launch_pass(m, dtype, in, out, none, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "pass_move launch");
+    return MOA_OK;
+}
+
 moa_status_t moa_fft_output_index(moa_fft_plan_t p, int64_t *pos, int64_t count) {
     if (!p || !pos) return fail(MOA_EINVAL, "output_index: null argument");
     if (p->is3d) return fail(MOA_EUNSUPPORTED, "output_index: 1-D plans only");
