@@ -354,6 +354,36 @@ def main():
         e2e = {"value": round(flops / (ems * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": data_bytes, "d2h_bytes_per_step": data_bytes, "ms_per_step": round(ems, 3)}
 
+    # latency of one exec (small, latency-bound plans -- cfg1): plain launches
+    # vs one CUDA-graph replay, warm L2, median of 200
+    latency = None
+    if small and not partitioned and rank == 0:
+        def med(fn, reps=200):
+            ts = []
+            for _ in range(reps):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                a1.record(stream)
+                a1.synchronize()
+                ts.append(a0.elapsed_time(a1) * 1e3)
+            return round(sorted(ts)[len(ts) // 2], 2)
+        plain_us = med(lambda: plan.exec(x, y, stream))
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                plan.exec(x, y, side)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=side):
+                    plan.exec(x, y, side)
+            stream.wait_stream(side)
+            graph_us = med(g.replay)
+        except Exception as ex:  # pragma: no cover
+            graph_us = f"capture failed: {ex}"
+        latency = {"plain_launch_us": plain_us, "cuda_graph_us": graph_us, "l2": "warm", "reps": 200}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gf, sample, thr = oracle_sample(args.workload, budget_s=12.0)
@@ -367,6 +397,8 @@ def main():
                f"inputs larger than L2 ({data_bytes / 2**30:.2f} GiB in + out per rank)",
                "parallelism": (f"processor-lifted over {world} ranks (NCCL all-to-all)" if partitioned else
                                (f"{world} independent replicas" if dist else "1 GPU"))}
+        if latency:
+            cfg["latency"] = latency
         if w["kind"] == "1d":
             cfg.update(n=w["n"], batch=w["batch"])
         else:
