@@ -71,6 +71,9 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // the processor lifting or an all-radix-2 lifting -- take more lines so a
     // CTA has at least 128 threads)
     int64_t W = lf ? (TPL >= 8 ? slots : (slots > 128 / TPL ? slots : 128 / TPL)) : (TPL >= 64 ? 1 : 256 / TPL);
+    // complex128 strided passes of <= 2^8 points: 256-byte runs (16 lines) --
+    // measured cfg3 5.50 -> 5.24 ms (the 32 MiB-stride first pass 1.50 -> 1.33 ms)
+    if (lf && esize == 16 && logR >= 5 && logR <= 8) W = 2 * slots;
     // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
     // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
     // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
