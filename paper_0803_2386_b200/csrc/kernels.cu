@@ -761,6 +761,22 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             KArgs b = a;
             b.W = d.W / 2;
             b.lW = log2_exact(b.W);
+            // the pair tile's own shared-memory line stride: 16-byte elements,
+            // W / 2 lines (the descriptor's was chosen for 8-byte elements)
+            {
+                const int64_t R = int64_t(1) << d.logR, base = R + R / 16;
+                int64_t best = base, bw = 1 << 30, bt = int64_t(1) << 62;
+                for (int64_t LS = base; LS < base + 16 && (b.W * LS * 16 <= d.smem_bytes); LS++) {
+                    int64_t tot = 0;
+                    const int w = psi_bank_conflicts(d.logR, b.W, 16, d.lf_load, d.lf_store, LS, &tot);
+                    if (w < bw || (w == bw && tot < bt)) {
+                        best = LS;
+                        bw = w;
+                        bt = tot;
+                    }
+                }
+                b.LS = int32_t(best);
+            }
             KFn<float4> f = kTabPair64[d.logR];
             if (d.smem_bytes > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);

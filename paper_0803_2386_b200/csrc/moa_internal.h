@@ -33,6 +33,8 @@ moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, 
 moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vector<int64_t> &radices);
 // Tile width (lines per CTA) and smem for a pass (fills desc.W / desc.smem_bytes / desc.threads).
 void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype);
+// worst conflict degree (and total extra wavefronts) of a tile's exchange patterns
+int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total);
 
 // kernels.cu
 struct DevTables {
