@@ -135,7 +135,10 @@ moa_status_t moa_fft_output_index(moa_fft_plan_t plan, int64_t *pos, int64_t cou
  * (a cudaStream_t of the plan's device; NULL = legacy default stream).
  *   in  : device pointer, `local elements` complex values (n*batch at ngpu=1),
  *         16-byte aligned.  Not modified unless in == out.
- *   out : device pointer, same size, 16-byte aligned; in == out is allowed.
+ *   out : device pointer, same size, 16-byte aligned; in == out is allowed
+ *         (plans whose first pass stores elsewhere than it loads -- the
+ *         rotating 3-D layouts, the unblocked control's bit reversal -- then
+ *         copy the input once into a plan-owned buffer, allocated on first use).
  * Returns without a host synchronisation; buffers must stay valid until the
  * stream passes the exec.  NULL or misaligned pointers -> MOA_EINVAL.
  */

@@ -51,6 +51,8 @@ struct moa_fft_plan_s {
     int64_t local_elems = 0;
     size_t esize = 16;
     uint32_t flags = 0;              // MOA_FFT_INVERSE / _NORMALIZE / _LIFTED_ORDER
+    bool inplace_safe = true;        // in == out works without a staging copy (see finish_plan)
+    void *inplace_buf = nullptr;     // the input copy of an in-place exec of an unsafe plan (lazy)
     bool lifted_out = false;         // one GPU: the last pass stores in place (no final transpose)
     moa_pass_desc_t natural_last{};  // ... and this is the natural-order descriptor it replaced
     std::vector<moa_pass_desc_t> passes;
@@ -201,6 +203,15 @@ moa_status_t finish_plan(moa_fft_plan_s *p) {
         e = kernel_attributes(p->dtype, d.logR, &mt, &regs);
         if (e != cudaSuccess) return cuda_fail(e, "kernel attributes (is the GPU an sm_100 part?)");
         if (d.threads > mt) return fail(MOA_EUNSUPPORTED, "pass tile exceeds the kernel's thread limit");
+    }
+    // in == out: safe unless a pass reads `in` and writes `out` at other
+    // positions than it read (a transposing store, the bit reversal) -- then
+    // exec stages the input through a plan-owned copy first
+    for (auto &d : p->passes) {
+        if (d.src != 0 || d.dst != 1) continue;
+        bool same = d.kind <= 1 && d.in_kstr == d.out_kstr && d.out_ksplit >= d.logR && !d.ring;
+        for (int i = 0; i < d.ndig && same; i++) same = d.in_str[i] == d.out_str[i];
+        if (!same) p->inplace_safe = false;
     }
     bool need_scratch = false;
     for (auto &d : p->passes) need_scratch |= (d.src == 2 || d.dst == 2);
@@ -426,6 +437,16 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (dev != p->device) return fail(MOA_EINVAL, "exec: the current device is not the plan's device");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (in == out && !p->inplace_safe) {  // stage the input (one device copy) so no pass reads what it overwrites
+        const size_t bytes = size_t(p->local_elems) * p->esize;
+        if (!p->inplace_buf) {
+            moa_status_t st = dev_alloc(p, bytes, &p->inplace_buf);
+            if (st) return st;
+        }
+        e = cudaMemcpyAsync(p->inplace_buf, in, bytes, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "exec: in-place staging copy");
+        in = p->inplace_buf;
+    }
     cudaEvent_t *evs = nullptr;
     if (p->prof_count < p->prof_max) evs = &p->prof_ev[size_t(p->prof_count) * (p->prof_nsteps + 1)];
     moa_status_t st = MOA_OK;

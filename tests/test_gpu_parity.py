@@ -130,10 +130,16 @@ def test_identity_and_tiny(m, torch_cuda):
         assert rel_l2(y, ref) <= TOL[dtype]
 
 
-def test_in_place_and_determinism(m, torch_cuda):
-    for n, batch in [(1 << 10, 4), (1 << 16, 3), (1 << 21, 1)]:
-        x = synth.fill(n * batch, 11, synth.UNIFORM)
-        plan = m.FFTPlan(n, batch, "c128")
+def test_in_place_and_determinism(m, torch_cuda, monkeypatch):
+    plans = [(lambda n=n, b=b: m.FFTPlan(n, b, "c128"), n * b) for n, b in [(1 << 10, 4), (1 << 16, 3), (1 << 21, 1)]]
+    plans += [(lambda: m.FFTPlan(1 << 12, 2, "c128", unblocked=True), 1 << 13),      # gather (bit reversal) first
+              (lambda: m.FFTPlan(1 << 14, 2, "c128", lifted_order=True), 1 << 15),
+              (lambda: m.FFTPlan.plan_3d(16, 32, 64, "c128"), 16 * 32 * 64),          # rotating layouts
+              (lambda: m.FFTPlan.plan_3d(16, 32, 64, "c64"), 16 * 32 * 64)]
+    for make, size in plans:
+        plan = make()
+        dt = "c64" if plan.dtype == m.MOA_C64 else "c128"
+        x = synth.fill(size, 11, synth.UNIFORM, dt)
         y1 = gpu_run(torch_cuda, plan, x)
         y2 = gpu_run(torch_cuda, plan, x, inplace=True)
         y3 = gpu_run(torch_cuda, plan, x)
