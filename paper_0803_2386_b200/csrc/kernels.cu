@@ -382,7 +382,18 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         const int64_t e0 = te + a.tw_off;
         double2 w = tw_lookup(hi, lo, (e0 * tB) & a.twmask, a.twh);
         const double2 ws = tw_lookup(hi, lo, (e0 * TPL) & a.twmask, a.twh);
-        if constexpr (LPL == 1) {
+        if constexpr (std::is_same<V, float2>::value) {
+            // complex64: the chain in fp32 from fp64-exact endpoints (<= 15
+            // products, ~1e-6 relative against a 2e-5 tolerance) -- no fp64
+            // multiplies or conversions per point
+            float2 wf = cvt_tw(w, V{});
+            const float2 wsf = cvt_tw(ws, V{});
+#pragma unroll
+            for (int m = 0; m < P; m++) {
+                pts[m] = cmul(pts[m], wf);
+                if (m + 1 < P) wf = cmul(wf, wsf);
+            }
+        } else if constexpr (LPL == 1) {
 #pragma unroll
             for (int m = 0; m < P; m++) {
                 pts[m] = cmul(pts[m], cvt_tw(w, V{}));
