@@ -287,7 +287,6 @@ __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int l
 
 __device__ __forceinline__ double2 cvt_tw(double2 w, double2) { return w; }
 __device__ __forceinline__ float2 cvt_tw(double2 w, float2) { return make_float2(float(w.x), float(w.y)); }
-__device__ __forceinline__ float2 cvt_tw(double2 w, float4) { return make_float2(float(w.x), float(w.y)); }
 
 // w_N^e from the two-level double-precision table (exact integer exponent)
 __device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, const double2 *__restrict__ lo, int64_t e,

@@ -153,7 +153,7 @@ int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t
         for (int64_t w0 = 0; w0 < nthr && w0 < 256; w0 += 32)
             for (int ph = 0; ph < 32; ph += per) {
                 int64_t seen[32];
-                int ns = 0, deg[32] = {0};
+                int ns = 0;
                 int64_t bank[32];
                 for (int ln = ph; ln < ph + per; ln++) {
                     const int64_t tid = w0 + ln;
@@ -170,7 +170,6 @@ int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t
                 for (int k = 0; k < ns; k++) {
                     int c = 0;
                     for (int q = 0; q < ns; q++) c += bank[q] == bank[k];
-                    deg[k] = c;
                     if (c > dmax) dmax = c;
                 }
                 if (dmax > worst) worst = dmax;
