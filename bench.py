@@ -306,8 +306,10 @@ def main():
             else:
                 launches_l.append(("pass", f"pass_kernel<{vt},{desc[i]['logR']}>"))
                 i += 1
-    kinds = [k for k, _ in launches_l]
     per_step = [s / max(nexec, 1) for s in step_ms_list]
+    if len(launches_l) != len(per_step):   # (e.g. a plan that fell back from fused to NCCL exchanges)
+        launches_l = [("pass", f"step {i}") for i in range(len(per_step))]
+    kinds = [k for k, _ in launches_l]
     pass_idx = [i for i, k in enumerate(kinds) if k in ("pass", "pair")]
     if not pass_idx:
         pass_idx = [i for i, k in enumerate(kinds) if k == "fused"]
