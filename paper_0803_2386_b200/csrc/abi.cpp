@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.h"
 #include "moa_internal.h"
 
@@ -27,6 +29,26 @@ moa_status_t fail(moa_status_t st, const std::string &msg) {
 static moa_status_t cuda_fail(cudaError_t e, const char *what) {
     return fail(MOA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// Tracing: with MOA_FFT_NVTX=1 every exec and every pass is an
+// NVTX range ("moa exec", "pass p R=.."), visible to Nsight Systems / ncu
+// --nvtx filters; a no-op otherwise.
+static bool nvtx_on() {
+    static const bool on = [] {
+        const char *e = std::getenv("MOA_FFT_NVTX");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const std::string &name) : on(nvtx_on()) {
+        if (on) nvtxRangePushA(name.c_str());
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+};
 
 PassMods pass_mods(uint32_t flags, size_t i, size_t npass, int64_t N) {
     PassMods m;
@@ -451,6 +473,7 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     if (p->prof_count < p->prof_max) evs = &p->prof_ev[size_t(p->prof_count) * (p->prof_nsteps + 1)];
     moa_status_t st = MOA_OK;
     const size_t np = p->passes.size();
+    NvtxRange exec_range(nvtx_on() ? "moa exec n=" + std::to_string(p->n) : std::string());
     if (p->dist) {
         st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs, p->flags, p->n);
     } else {
@@ -458,6 +481,8 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
         for (size_t i = 0; i < np; i++, step++) {
             const moa_pass_desc_t &d = p->passes[i];
             const void *src = d.src == 0 ? in : d.src == 1 ? static_cast<const void *>(out) : p->scratch;
+            NvtxRange pass_range(nvtx_on() ? "pass " + std::to_string(i) + " R=" + std::to_string(1 << d.logR)
+                                           : std::string());
             if (evs) cudaEventRecord(evs[step], s);
             if (d.ring == 2) {  // fused pair: passes i and i+1 in one launch, intermediate in the L2 ring
                 const moa_pass_desc_t &dB = p->passes[i + 1];
