@@ -113,6 +113,23 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def host_info():
+    """CPU model, logical CPUs and RAM of the host the oracle runs on."""
+    model, mem = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "host_ram_gib": mem}
+
+
 def oracle_sample(wname, budget_s):
     """Time the oracle (as it stands) on a bounded sample of the workload.
     -> (GFLOP/s, sample description, threads)."""
@@ -177,7 +194,7 @@ def run_reference(args, w, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{wname}: {w['desc']}"},
         "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, **host_info()},
         "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -360,7 +377,7 @@ def main():
     # vs one CUDA-graph replay, warm L2, median of 200
     latency = None
     if small and not partitioned and rank == 0:
-        def med(fn, reps=200):
+        def med(fn, reps=1000):
             ts = []
             for _ in range(reps):
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -384,12 +401,13 @@ def main():
             graph_us = med(g.replay)
         except Exception as ex:  # pragma: no cover
             graph_us = f"capture failed: {ex}"
-        latency = {"plain_launch_us": plain_us, "cuda_graph_us": graph_us, "l2": "warm", "reps": 200}
+        latency = {"plain_launch_us": plain_us, "cuda_graph_us": graph_us, "l2": "warm", "reps": 1000}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gf, sample, thr = oracle_sample(args.workload, budget_s=12.0)
-        cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle", "sample": sample}
+        cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle", "sample": sample,
+               **host_info()}
 
     if rank == 0:
         cfg = {"workload": f"{args.workload}: {w['desc']}", "dtype_elem": w["dtype"],
