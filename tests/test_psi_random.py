@@ -81,3 +81,31 @@ def test_random_liftings_on_gpu(radices, batch, dtype):
     got = y.cpu().numpy().astype(np.complex128)
     tol = 1e-11 if dtype == "c128" else 2e-5
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= tol
+
+
+# ---------------------------------------------------------------- processor-level lifting, random
+@settings(max_examples=25, deadline=None)
+@given(p=st.sampled_from([2, 4, 8]), t=st.integers(min_value=6, max_value=14),
+       lifted=st.booleans(), peer=st.sampled_from(["0", "1"]), dtype=st.sampled_from(["c128", "c64"]))
+def test_random_distributed_schedules(p, t, lifted, peer, dtype):
+    import os
+    from onf import run_dist
+    N = 1 << t
+    if N < p * p:
+        return
+    old = os.environ.get("MOA_FFT_PEER")
+    os.environ["MOA_FFT_PEER"] = peer
+    try:
+        flags = m.MOA_FFT_LIFTED_ORDER if lifted else 0
+        sch = [m.moa_dist_describe(r, p, N, dtype, flags=flags) for r in range(p)]
+    finally:
+        if old is None:
+            os.environ.pop("MOA_FFT_PEER", None)
+        else:
+            os.environ["MOA_FFT_PEER"] = old
+    x = synth.fill(N, 34, synth.UNIFORM)
+    outs = run_dist(sch, np.split(x, p))
+    ref = oracle.fft_radix2(x)
+    for g in range(p):
+        want = ref[g::p] if lifted else ref[g * (N // p):(g + 1) * (N // p)]
+        assert np.linalg.norm(outs[g] - want) / np.linalg.norm(want) < 1e-12
