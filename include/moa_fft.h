@@ -271,6 +271,32 @@ moa_status_t moa_psi_describe_3d(int64_t n0, int64_t n1, int64_t n2, moa_dtype_t
 moa_status_t moa_plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, int64_t *radices, int max_rad,
                               int *nrad);
 /*
+ * Density-matrix gate (PAPER.md Ch.6, "Density Matrix Operations for a Quantum
+ * Computer").  A 2^n x 2^n density matrix D
+ * (row-major, interleaved complex of `dtype`) is viewed as the 2n-cube D_h and
+ * transposed by the vector t that moves the gated bits to the diagonal; every
+ * 2^q x 2^q block of that view is replaced by U B U^dagger -- D <- U_full D
+ * U_full^dagger without forming U_full or any temporary (Eq. generic,
+ * i psi (t transpose D) = @D + gamma(i[t]; s)).
+ * Conventions: bit 0 is the least significant; hypercube position p of an
+ * n-bit half is bit n-1-p; bit j of U's row / column index is the j-th lowest
+ * gated bit; i[t] has component t[k] equal to i[k] (R15).
+ *
+ * moa_qgate_permutation -- t (2n entries) for gated_bits[0..q) (host only).
+ * moa_qgate_view_offset -- the element offset in D of view element
+ *   (view_row, view_col): Eq. generic (host only).
+ * moa_qgate_apply -- in place on the device matrix rho (16-byte aligned),
+ *   stream-ordered; u is a HOST array of 2^q x 2^q complex values (row-major,
+ *   same dtype as rho), copied at the call.  1 <= n <= 15, 1 <= q <= min(3, n),
+ *   gated bits distinct in [0, n); otherwise MOA_EINVAL.
+ */
+moa_status_t moa_qgate_permutation(int n, const int32_t *gated_bits, int q, int32_t *t);
+moa_status_t moa_qgate_view_offset(int n, const int32_t *gated_bits, int q, int64_t view_row, int64_t view_col,
+                                   int64_t *offset);
+moa_status_t moa_qgate_apply(void *rho, int n, const int32_t *gated_bits, int q, const void *u, moa_dtype_t dtype,
+                             void *stream);
+
+/*
  * moa_pass_move -- test hook: execute ONE pass descriptor as a
  * pure data movement on the GPU -- kind forced to 1 (no DFT), no twiddle, no
  * ring -- so that out[store(line, k)] = in[load(line, k)] for every line and

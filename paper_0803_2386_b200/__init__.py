@@ -29,6 +29,7 @@ EXPORTS = [
     "moa_fft_exec_loopback", "moa_dist_describe", "moa_psi_describe", "moa_psi_describe_3d",
     "moa_plan_radices", "moa_fft_plan_describe", "moa_fft_prof_begin", "moa_fft_prof_end",
     "moa_fft_plan_ex", "moa_fft_plan_3d_ex", "moa_fft_output_index", "moa_pass_move",
+    "moa_qgate_permutation", "moa_qgate_view_offset", "moa_qgate_apply",
 ]
 
 
@@ -95,6 +96,9 @@ def _load():
         "moa_fft_plan_3d_ex": [P(vp), i64, i64, i64, i32, i32, ctypes.c_uint32],
         "moa_fft_output_index": [vp, P(i64), i64],
         "moa_pass_move": [P(PassDesc), i32, vp, vp, vp],
+        "moa_qgate_permutation": [i32, P(ctypes.c_int32), i32, P(ctypes.c_int32)],
+        "moa_qgate_view_offset": [i32, P(ctypes.c_int32), i32, i64, i64, P(i64)],
+        "moa_qgate_apply": [vp, i32, P(ctypes.c_int32), i32, vp, i32, vp],
         "moa_fft_exec": [vp, vp, vp, vp],
         "moa_fft_exec_host": [vp, vp, vp, vp],
         "moa_fft_destroy": [vp],
@@ -176,6 +180,33 @@ def moa_pass_move(desc: dict, dtype, in_ptr: int, out_ptr: int, stream: int = 0)
     pure data movement on the GPU (see include/moa_fft.h)."""
     d = PassDesc.from_dict(desc)
     _check(lib.moa_pass_move(ctypes.byref(d), _dt(dtype), in_ptr, out_ptr, stream))
+
+
+def moa_qgate_permutation(n: int, gated_bits) -> list:
+    """The Ch.6 transpose vector t (2n entries) moving the gated bits to the diagonal."""
+    bits = (ctypes.c_int32 * len(gated_bits))(*gated_bits)
+    t = (ctypes.c_int32 * (2 * n))()
+    _check(lib.moa_qgate_permutation(n, bits, len(gated_bits), t))
+    return list(t)
+
+
+def moa_qgate_view_offset(n: int, gated_bits, view_row: int, view_col: int) -> int:
+    bits = (ctypes.c_int32 * len(gated_bits))(*gated_bits)
+    off = ctypes.c_int64()
+    _check(lib.moa_qgate_view_offset(n, bits, len(gated_bits), view_row, view_col, ctypes.byref(off)))
+    return off.value
+
+
+def moa_qgate_apply(rho, n: int, gated_bits, u, stream=None) -> None:
+    """D <- U_full D U_full^dagger in place on the CUDA tensor rho (2^n x 2^n,
+    complex64/complex128); u: the 2^q x 2^q gate (numpy / host)."""
+    import numpy as np
+    import torch
+    dt = MOA_C128 if rho.dtype == torch.complex128 else MOA_C64
+    uh = np.ascontiguousarray(u, dtype=np.complex128 if dt == MOA_C128 else np.complex64)
+    bits = (ctypes.c_int32 * len(gated_bits))(*gated_bits)
+    s = stream if stream is not None else torch.cuda.current_stream(rho.device)
+    _check(lib.moa_qgate_apply(rho.data_ptr(), n, bits, len(gated_bits), uh.ctypes.data, dt, s.cuda_stream))
 
 
 def moa_fft_plan_lift(n: int, batch: int, dtype, radices) -> int:

@@ -242,3 +242,25 @@ def test_fused_pair_descriptors_compute_the_dft(monkeypatch):
     # cfg2's plan is one fused launch
     p2 = m.moa_psi_describe(1 << 16, 1024, "c128")
     assert [d["ring"] for d in p2] == [2, 1]
+
+
+# ---------------------------------------------------------------- Ch.6 density-matrix gate (host side)
+def test_qgate_transpose_vector_and_view_offsets_bit_exact_vs_oracle():
+    from oracle import qgate
+    assert m.moa_qgate_permutation(4, [0, 2]) == [0, 2, 1, 3, 4, 6, 5, 7]
+    assert m.moa_qgate_permutation(4, [1, 2]) == [0, 3, 1, 2, 4, 7, 5, 6]
+    rng = np.random.default_rng(4)
+    for n in range(1, 8):
+        for _ in range(4):
+            q = int(rng.integers(1, min(3, n) + 1))
+            bits = [int(b) for b in rng.choice(n, q, replace=False)]
+            t = m.moa_qgate_permutation(n, bits)
+            assert t == qgate.gate_permutation(n, bits)
+            N = 1 << n
+            for vr in range(N):
+                for vc in range(N):
+                    i_vec = [(vr >> (n - 1 - p)) & 1 for p in range(n)] + [(vc >> (n - 1 - p)) & 1 for p in range(n)]
+                    assert m.moa_qgate_view_offset(n, bits, vr, vc) == qgate.permuted_offset(i_vec, t)
+    for bad in [(4, [4]), (4, [1, 1]), (0, [0]), (4, [0, 1, 2, 3])]:
+        with pytest.raises(m.MoaError):
+            m.moa_qgate_permutation(*bad)
