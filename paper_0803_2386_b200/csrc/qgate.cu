@@ -17,8 +17,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "../../include/moa_fft.h"
 #include "moa_internal.h"
@@ -27,15 +31,19 @@ namespace moa {
 namespace {
 
 constexpr int kMaxQ = 8;      // 2^q, q <= 3
-constexpr int kMaxTC = 128;   // tile columns (threads per CTA)
+constexpr int kMaxTC = 256;   // tile columns (threads per CTA)
+// S holds two Q x (TC + 1) buffers: cap TC so that stays near 32 KiB for complex128
+constexpr __host__ __device__ int tc_cap(int Q) { return Q <= 4 ? 256 : 128; }
 
 template <typename V> struct QgArgs {
     V *rho;
     int64_t N;                 // 2^n
     int32_t Q, TC;             // 2^q, tile columns = Q * K
+    int32_t RG;                // ungated row indices per CTA (consecutive)
+    int32_t TP;                // shared-memory row stride (elements), >= TC
     int64_t gdep[kMaxQ];       // pdep(a, gated mask), a < Q
     int32_t vdep[kMaxTC];      // pdep(tc, varying column mask), tc < TC
-    int32_t bsel[kMaxTC];      // gated part b of tile column tc (pext over the gated positions)
+    int32_t rdep[kMaxTC];      // tile column of the rest index ri with all gated values 0, ri < TC / Q
     int32_t gpos_dep[kMaxQ];   // tile-column offset of gated value l (pdep(l, gated positions in tc))
     int32_t gpos_mask;         // positions of the gated bits inside tc
     uint32_t ung_mask;         // ungated bits (rows: all of them)
@@ -55,62 +63,85 @@ __device__ __forceinline__ int64_t pdep_loop(int64_t x, uint32_t mask) {
     return r;
 }
 
-__device__ __forceinline__ double2 cmulq(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+// acc + a * b and acc + a * conj(b) as four FMAs (the gate is FP64-FMA bound at q = 3)
+template <typename V> __device__ __forceinline__ void cmac(V &acc, V a, V b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
 }
-__device__ __forceinline__ float2 cmulq(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cmulcq(double2 a, double2 b) {  // a * conj(b)
-    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
-}
-__device__ __forceinline__ float2 cmulcq(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
-}
-template <typename V> __device__ __forceinline__ V caddq(V a, V b) {
-    V r;
-    r.x = a.x + b.x;
-    r.y = a.y + b.y;
-    return r;
+template <typename V> __device__ __forceinline__ void cmacc(V &acc, V a, V b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.y, b.x, acc.y);
+    acc.y = fma(-a.x, b.y, acc.y);
 }
 
 template <typename V, int Q>
-__global__ void __launch_bounds__(kMaxTC) qgate_kernel(const __grid_constant__ QgArgs<V> a) {
-    __shared__ V S[Q][kMaxTC];
-    __shared__ V T[Q][kMaxTC];
+__global__ void __launch_bounds__(tc_cap(Q)) qgate_kernel(const __grid_constant__ QgArgs<V> a) {
+    // One row group = the Q x TC tile B of Q view rows; per row group:
+    //   stage    S[k][tc]  <- B[k][tc]              (thread tc; coalesced rows)
+    //   phase 1  S[k][rest | j] <- sum_l S[k][rest | l] conj(U[j][l])   (T = B U^dagger;
+    //            thread (k, ri) owns the Q entries it reads and writes -> in place)
+    //   phase 2  B'[i][tc] = sum_k U[i][k] S[k][tc]  (thread tc; coalesced stores)
+    // Every element crosses shared memory twice each way; U is read with
+    // warp-uniform indices.  S is double-buffered (dynamic shared memory, row
+    // stride a.TP chosen on the host by a bank model of the phase-1 pattern; the
+    // row-contiguous stage / phase-2 accesses are conflict-free for any stride):
+    // iteration it uses buffer it & 1, last used by iteration it - 2, whose
+    // phase-2 reads all precede iteration it - 1's first barrier.
+    extern __shared__ __align__(16) unsigned char qg_smem[];
+    const int TP = a.TP;
     const int tc = threadIdx.x;
-    // CTA -> (r: ungated row index, h: ungated column index above the tile)
-    const int64_t nh = a.N / (int64_t(Q) * (a.TC / Q));  // column tiles per row
-    const int64_t r = blockIdx.x / nh, h = blockIdx.x % nh;
-    const int64_t row0 = pdep_loop(r, a.ung_mask);
+    const int64_t nh = a.N / a.TC;  // column tiles per row
+    const int64_t rg = blockIdx.x / nh, h = blockIdx.x % nh;
     const int64_t col = pdep_loop(h, a.ung_hi_mask) + a.vdep[tc];
-    V *base = a.rho + row0 * a.N + col;
-    // gather the Q view rows of this tile (each row a coalesced run of columns)
+    const int k1 = tc & (Q - 1);       // phase-1 row
+    const int rest = a.rdep[tc / Q];   // phase-1 column base (gated values 0)
+    const int64_t ung = int64_t(a.ung_mask);
+    int64_t row0 = pdep_loop(rg * a.RG, a.ung_mask);
+    V cur[Q];
 #pragma unroll
-    for (int k = 0; k < Q; k++) S[k][tc] = base[a.gdep[k] * a.N];
-    __syncthreads();
-    // T = B U^dagger : T[k][tc] = sum_l B[k][(tc, l)] conj(U[b][l])
-    const int b = a.bsel[tc];
-    const int rest = tc & ~a.gpos_mask;
+    for (int k = 0; k < Q; k++) cur[k] = a.rho[(row0 + a.gdep[k]) * a.N + col];
+    for (int it = 0; it < a.RG; it++) {
+        V *Sb = reinterpret_cast<V *>(qg_smem) + (it & 1) * Q * TP;
 #pragma unroll
-    for (int k = 0; k < Q; k++) {
-        V acc;
-        acc.x = 0;
-        acc.y = 0;
+        for (int k = 0; k < Q; k++) Sb[k * TP + tc] = cur[k];
+        const int64_t next = ((row0 | ~ung) + 1) & ung;  // pdep(r + 1, ung) from pdep(r, ung)
+        if (it + 1 < a.RG) {
 #pragma unroll
-        for (int l = 0; l < Q; l++) acc = caddq(acc, cmulcq(S[k][rest | a.gpos_dep[l]], a.u[b * Q + l]));
-        T[k][tc] = acc;
-    }
-    __syncthreads();
-    // B' = U T, written back in place
+            for (int k = 0; k < Q; k++) cur[k] = a.rho[(next + a.gdep[k]) * a.N + col];
+        }
+        __syncthreads();
+        {
+            V x[Q];
 #pragma unroll
-    for (int i = 0; i < Q; i++) {
-        V acc;
-        acc.x = 0;
-        acc.y = 0;
+            for (int l = 0; l < Q; l++) x[l] = Sb[k1 * TP + (rest | a.gpos_dep[l])];
 #pragma unroll
-        for (int k = 0; k < Q; k++) acc = caddq(acc, cmulq(a.u[i * Q + k], T[k][tc]));
-        base[a.gdep[i] * a.N] = acc;
+            for (int j = 0; j < Q; j++) {
+                V acc;
+                acc.x = 0;
+                acc.y = 0;
+#pragma unroll
+                for (int l = 0; l < Q; l++) cmacc(acc, x[l], a.u[j * Q + l]);
+                Sb[k1 * TP + (rest | a.gpos_dep[j])] = acc;
+            }
+        }
+        __syncthreads();
+        V *base = a.rho + row0 * a.N + col;
+        V t[Q];
+#pragma unroll
+        for (int k = 0; k < Q; k++) t[k] = Sb[k * TP + tc];
+#pragma unroll
+        for (int i = 0; i < Q; i++) {
+            V acc;
+            acc.x = 0;
+            acc.y = 0;
+#pragma unroll
+            for (int k = 0; k < Q; k++) cmac(acc, a.u[i * Q + k], t[k]);
+            base[a.gdep[i] * a.N] = acc;
+        }
+        row0 = next;
     }
 }
 
@@ -137,6 +168,55 @@ int64_t pdep_host(int64_t x, uint32_t mask) {
     return r;
 }
 
+// Shared-memory wavefronts of one phase-1 access (lane (k1, ri) of warp w
+// touching S[k1 * TP + (rdep[ri] | gpos_dep[l])]): the lanes are served in
+// groups of 128 bytes (8 lanes for 16-byte elements, 16 for 8-byte), each
+// group taking max over the 32 four-byte banks of the words it hits.  The
+// stride is the TP in [TC, TC + 32) with the fewest wavefronts summed over
+// groups, warps and l (ties: smallest).  Measured (profiles/r1_s6_qgate_tp.jsonl):
+// a whole-warp bank count ties TC with TC + 2 for gated bits {3, 9} while TC
+// runs 25 % slower; the per-group count separates them.
+int qgate_row_stride(int Q, int TC, const int32_t *rdep, const int32_t *gpos_dep, int esz) {
+    // memoised per (Q, TC, gated positions in the tile, element size)
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int>, int> memo;
+    const auto key = std::make_tuple(Q, TC, gpos_dep[Q - 1], esz);  // gpos_dep[Q - 1] = the gated-position mask
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = memo.find(key);
+        if (it != memo.end()) return it->second;
+    }
+    const int words = esz / 4;
+    int best_tp = TC;
+    long best = -1;
+    for (int tp = TC; tp < TC + 32; tp++) {
+        long cost = 0;
+        for (int w = 0; w < TC / 32; w++)
+            for (int l = 0; l < Q; l++) {
+                // distinct lanes hit distinct elements (each (k1, ri) owns its own)
+                const int grp = 32 / words;
+                for (int g0 = 0; g0 < 32; g0 += grp) {
+                    int per_bank[32] = {0};
+                    for (int lane = g0; lane < g0 + grp; lane++) {
+                        const int tc = w * 32 + lane;
+                        const int e = (tc & (Q - 1)) * tp + (rdep[tc / Q] | gpos_dep[l]);
+                        for (int x = 0; x < words; x++) per_bank[(e * words + x) & 31]++;
+                    }
+                    int mx = 0;
+                    for (int b = 0; b < 32; b++) mx = per_bank[b] > mx ? per_bank[b] : mx;
+                    cost += mx;
+                }
+            }
+        if (best < 0 || cost < best) {
+            best = cost;
+            best_tp = tp;
+        }
+    }
+    std::lock_guard<std::mutex> g(mu);
+    memo[key] = best_tp;
+    return best_tp;
+}
+
 template <typename V>
 moa_status_t qgate_launch(V *rho, int n, uint32_t gmask, int q, const V *u, cudaStream_t s) {
     QgArgs<V> a;
@@ -146,7 +226,7 @@ moa_status_t qgate_launch(V *rho, int n, uint32_t gmask, int q, const V *u, cuda
     const uint32_t ung = all & ~gmask;
     // tile: all Q gated column values x K = 2^kc lowest ungated column values
     int kc = 0;
-    while ((Q << (kc + 1)) <= kMaxTC && kc + 1 <= n - q) kc++;
+    while ((Q << (kc + 1)) <= tc_cap(Q) && kc + 1 <= n - q) kc++;
     uint32_t low_ung = 0;
     {
         int taken = 0;
@@ -171,21 +251,25 @@ moa_status_t qgate_launch(V *rho, int n, uint32_t gmask, int q, const V *u, cuda
         if (gmask & (1u << bit)) a.gpos_mask |= 1 << pos;
         pos++;
     }
-    for (int tc = 0; tc < a.TC; tc++) {
-        a.vdep[tc] = int32_t(pdep_host(tc, vmask));
-        int b = 0, j = 0;
-        for (int p = 0; p < 16; p++)
-            if (a.gpos_mask & (1 << p)) b |= ((tc >> p) & 1) << j++;
-        a.bsel[tc] = b;
-    }
+    for (int tc = 0; tc < a.TC; tc++) a.vdep[tc] = int32_t(pdep_host(tc, vmask));
+    for (int ri = 0; ri < a.TC / Q; ri++)
+        a.rdep[ri] = int32_t(pdep_host(ri, uint32_t(a.TC - 1) & ~uint32_t(a.gpos_mask)));
     for (int l = 0; l < Q; l++) a.gpos_dep[l] = int32_t(pdep_host(l, uint32_t(a.gpos_mask)));
     for (int i = 0; i < Q * Q; i++) a.u[i] = u[i];
-    const int64_t blocks = (a.N / Q) * (a.N / a.TC);
+    // several row groups per CTA (about 8 K elements of work per CTA)
+    const int64_t rows_groups = a.N / Q;
+    int64_t rgp = 1;
+    while (rgp * 2 <= rows_groups && rgp * 2 * Q * a.TC <= 8192) rgp *= 2;
+    a.RG = int32_t(rgp);
+    const int64_t blocks = (rows_groups / rgp) * (a.N / a.TC);
+    a.TP = qgate_row_stride(Q, a.TC, a.rdep, a.gpos_dep, int(sizeof(V)));
+    if (const char *e = std::getenv("MOA_QG_TP_OFF")) a.TP = a.TC + std::atoi(e);  // ablation knob
+    const size_t smem = size_t(2) * Q * a.TP * sizeof(V);
     if (blocks > 0x7fffffff) return fail(MOA_EUNSUPPORTED, "qgate: grid too large");
     switch (Q) {
-        case 2: qgate_kernel<V, 2><<<unsigned(blocks), a.TC, 0, s>>>(a); break;
-        case 4: qgate_kernel<V, 4><<<unsigned(blocks), a.TC, 0, s>>>(a); break;
-        default: qgate_kernel<V, 8><<<unsigned(blocks), a.TC, 0, s>>>(a); break;
+        case 2: qgate_kernel<V, 2><<<unsigned(blocks), a.TC, smem, s>>>(a); break;
+        case 4: qgate_kernel<V, 4><<<unsigned(blocks), a.TC, smem, s>>>(a); break;
+        default: qgate_kernel<V, 8><<<unsigned(blocks), a.TC, smem, s>>>(a); break;
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("qgate launch: ") + cudaGetErrorString(e));
