@@ -70,7 +70,7 @@ def test_planner_liftings():
     assert m.moa_plan_radices(1 << 10) == [1 << 10]
     assert m.moa_plan_radices(1 << 16) == [256, 256]
     assert m.moa_plan_radices(1 << 28, 1, "c128") == [128, 128, 128, 128]    # two fused pairs
-    assert m.moa_plan_radices(1 << 30, 1, "c64") == [256, 256, 128, 128]
+    assert m.moa_plan_radices(1 << 30, 1, "c64") == [256, 128, 128, 256]
     r3 = m.moa_plan_radices(1 << 27, 1, "c128")                              # odd t: three passes
     assert np.prod(r3) == 1 << 27 and len(r3) == 3 and max(r3[:-1]) <= 512
     for t in range(0, 34):
