@@ -439,10 +439,13 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     {
         const uint64_t pol = l2_policy(a.ring == 2);
         if (a.ksplit >= LR) {  // the common case: one affine stride per point
-            E *base = out + oo + int64_t(tB) * a.out_kstr;
-            const int64_t step = int64_t(TPL) * a.out_kstr;
+            char *ptr = reinterpret_cast<char *>(out + oo + int64_t(tB) * a.out_kstr);
+            const int64_t stepb = int64_t(TPL) * a.out_kstr * int64_t(sizeof(E));
 #pragma unroll
-            for (int m = 0; m < P; m++) st_pol(reinterpret_cast<V *>(base + m * step), pts[m], pol);
+            for (int m = 0; m < P; m++) {
+                st_pol(reinterpret_cast<V *>(ptr), pts[m], pol);
+                ptr += stepb;
+            }
         } else {
 #pragma unroll
             for (int m = 0; m < P; m++) st_pol(reinterpret_cast<V *>(out + oo + kaddr(a, tB + m * TPL)), pts[m], pol);
@@ -466,10 +469,15 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
     {
         const uint64_t pol = l2_policy(a.ring == 1);
-        const E *base = reinterpret_cast<const E *>(a.in) + io + int64_t(mp.tA) * a.in_kstr;
-        const int64_t step = int64_t(TPL) * a.in_kstr;
+        // byte-pointer increments: one 64-bit add per point (the element-index
+        // form costs an add and a scaled add per point)
+        const char *ptr = reinterpret_cast<const char *>(reinterpret_cast<const E *>(a.in) + io + int64_t(mp.tA) * a.in_kstr);
+        const int64_t stepb = int64_t(TPL) * a.in_kstr * int64_t(sizeof(E));
 #pragma unroll
-        for (int m = 0; m < P; m++) pts[m] = ld_pol(reinterpret_cast<const V *>(base + m * step), pol);
+        for (int m = 0; m < P; m++) {
+            pts[m] = ld_pol(reinterpret_cast<const V *>(ptr), pol);
+            ptr += stepb;
+        }
     }
     if (a.conj_in) {  // inverse transform: DFT of conj(x) (the plan's first pass)
 #pragma unroll
