@@ -331,6 +331,33 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     const TileMap mp = tile_map<TPL>(a);
     const int lA = mp.lA, tA = mp.tA, lB = mp.lB, tB = mp.tB;
 
+    // The lifted weights' two-level table entries (step 3 forms their
+    // products).  complex128: fetched here, ahead of the butterflies, so their
+    // L2 latency (2^28-point plans: 256 KiB tables) hides behind the block DFT
+    // (measured cfg3 5.25 -> 5.13 ms, 3-D 19.2 -> 18.8 ms; no occupancy cost at
+    // 2 CTAs/SM).  complex64: fetched in step 3 -- holding them costs 9
+    // registers and one CTA per SM (64 -> 73; cfg4 11.2 -> 12.0 ms).
+    constexpr bool kEarlyTw = std::is_same<V, double2>::value;
+    const int64_t te = b_te + int64_t(LPL * lB) * a.tw_str[0];
+    double2 tq[LPL][4];
+    auto fetch_tw = [&]() {
+        const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
+        const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
+        const int64_t lmask = (int64_t(1) << a.twh) - 1;
+#pragma unroll
+        for (int q = 0; q < LPL; q++) {  // the pair's second line has its own exponent base
+            const int64_t e0 = te + a.tw_off + q * a.tw_str[0];
+            const int64_t ea = (e0 * tB) & a.twmask, eb = (e0 * TPL) & a.twmask;
+            tq[q][0] = __ldg(hi + (ea >> a.twh));
+            tq[q][1] = __ldg(lo + (ea & lmask));
+            tq[q][2] = __ldg(hi + (eb >> a.twh));
+            tq[q][3] = __ldg(lo + (eb & lmask));
+        }
+    };
+    if constexpr (kEarlyTw) {
+        if (a.twmask) fetch_tw();
+    }
+
     // ---- 2. block butterflies (R-point DFT of every line); the mapping switches
     //         from A to B at the first shared-memory exchange
     bool moved = false;
@@ -373,14 +400,11 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     //         in double precision (<= 15 products, ~1e-15 relative)
     // (the W lines of a tile share every digit but digit 0, which W divides)
     int64_t oo = b_oo + int64_t(LPL * lB) * a.out_str[0];
-    const int64_t te = b_te + int64_t(LPL * lB) * a.tw_str[0];
     if (a.ring == 2) oo += ring_off;
     if (a.twmask) {
-        const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
-        const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
-        const int64_t e0 = te + a.tw_off;
-        double2 w = tw_lookup(hi, lo, (e0 * tB) & a.twmask, a.twh);
-        const double2 ws = tw_lookup(hi, lo, (e0 * TPL) & a.twmask, a.twh);
+        if constexpr (!kEarlyTw) fetch_tw();
+        double2 w = cmul(tq[0][0], tq[0][1]);
+        const double2 ws = cmul(tq[0][2], tq[0][3]);
         if constexpr (std::is_same<V, float2>::value) {
             // complex64: the chain in fp32 from fp64-exact endpoints (<= 15
             // products, ~1e-6 relative against a 2e-5 tolerance) -- no fp64
@@ -398,10 +422,9 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
                 pts[m] = cmul(pts[m], cvt_tw(w, V{}));
                 if (m + 1 < P) w = cmul(w, ws);
             }
-        } else {  // the pair's second line has its own exponent base
-            const int64_t e1 = e0 + a.tw_str[0];
-            double2 w1 = tw_lookup(hi, lo, (e1 * tB) & a.twmask, a.twh);
-            const double2 ws1 = tw_lookup(hi, lo, (e1 * TPL) & a.twmask, a.twh);
+        } else {  // the pair: the second line's chain
+            double2 w1 = cmul(tq[1][0], tq[1][1]);
+            const double2 ws1 = cmul(tq[1][2], tq[1][3]);
 #pragma unroll
             for (int m = 0; m < P; m++) {
                 pts[m] = cmul(pts[m], make_float4(float(w.x), float(w.y), float(w1.x), float(w1.y)));
