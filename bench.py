@@ -190,7 +190,11 @@ def run_reference(args, w, rank):
     v = float(np.median(vals))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup,
+        # one full step of the workload at the sampled rate (the oracle is timed
+        # on a bounded sample; see cpu_baseline.sample)
+        "ms_per_step": round(flops_per_step(w) / (v * 1e9) * 1e3, 3), "ms_per_step_basis": "extrapolated from the sample",
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{wname}: {w['desc']}"},
         "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": thr, "kind": "oracle",
