@@ -149,25 +149,50 @@ void fuse_exchanges(std::vector<DistStep> &steps, std::vector<moa_pass_desc_t> &
 }
 
 namespace {
+// One int per rank through the communicator (plan time only): the minimum over
+// ranks, or 0 if the reduction itself fails.
+int all_ranks_min(int v) {
+    int *d = nullptr;
+    int out = 0;
+    cudaStream_t s = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    bool ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMemcpy(d, &v, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+              g_nccl.allReduce(d, d, 1, ncclInt32, ncclMin, g_comm, s) == ncclSuccess &&
+              cudaStreamSynchronize(s) == cudaSuccess &&
+              cudaMemcpy(&out, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (s) cudaStreamDestroy(s);
+    cudaFree(d);
+    if (!ok) cudaGetLastError();
+    return ok ? out : 0;
+}
+
 // Map every rank's scratch buffer `id` into this process (CUDA IPC over
 // NVLink): the handles are all-gathered through the communicator at plan time.
+// Every rank takes part in the all-gather even when its own handle is missing
+// (a flag travels with the handle), so a local failure cannot leave the other
+// ranks waiting in a collective; the outcome is the same on every rank up to
+// the opens, which dist_finish reconciles with all_ranks_min.
 moa_status_t setup_peers(DistPlan *dp, int id, void *local) {
-    if (!g_nccl.allGather || !g_nccl.allReduce) return fail(MOA_EUNSUPPORTED, "NCCL lacks allGather/allReduce");
-    cudaIpcMemHandle_t h;
-    if (!local || cudaIpcGetMemHandle(&h, local) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(MOA_EUNSUPPORTED, "cudaIpcGetMemHandle failed");
-    }
-    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    struct Msg {
+        cudaIpcMemHandle_t h;
+        int ok;
+    } mine{};
+    mine.ok = local && cudaIpcGetMemHandle(&mine.h, local) == cudaSuccess;
+    if (!mine.ok) cudaGetLastError();
+    const size_t hb = sizeof(Msg);
     char *d = nullptr;
     if (cudaMalloc(&d, hb * dp->ngpu) != cudaSuccess) {
         cudaGetLastError();
         return fail(MOA_ENOMEM, "peer handle buffer");
     }
-    std::vector<char> all(hb * dp->ngpu);
+    std::vector<Msg> all(dp->ngpu);
     cudaStream_t s = nullptr;
     bool ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaMemcpy(d + hb * dp->rank, &h, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(d + hb * dp->rank, &mine, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
               g_nccl.allGather(d + hb * dp->rank, d, hb, ncclChar, g_comm, s) == ncclSuccess &&
               cudaStreamSynchronize(s) == cudaSuccess &&
               cudaMemcpy(all.data(), d, hb * dp->ngpu, cudaMemcpyDeviceToHost) == cudaSuccess;
@@ -177,20 +202,31 @@ moa_status_t setup_peers(DistPlan *dp, int id, void *local) {
         cudaGetLastError();
         return fail(MOA_ENCCL, "peer handle exchange failed");
     }
+    for (int g = 0; g < dp->ngpu; g++)
+        if (!all[g].ok) return fail(MOA_EUNSUPPORTED, "cudaIpcGetMemHandle failed on some rank");
     for (int g = 0; g < dp->ngpu; g++) {
         if (g == dp->rank) {
             dp->peer_buf[id][g] = local;
             continue;
         }
-        cudaIpcMemHandle_t ph;
-        std::memcpy(&ph, all.data() + hb * g, hb);
-        if (cudaIpcOpenMemHandle(&dp->peer_buf[id][g], ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        if (cudaIpcOpenMemHandle(&dp->peer_buf[id][g], all[g].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
             cudaGetLastError();
             return fail(MOA_EUNSUPPORTED, "cudaIpcOpenMemHandle failed (no peer access?)");
         }
         dp->peer_opened[id][g] = true;
     }
     return MOA_OK;
+}
+
+void close_peers(DistPlan *dp) {
+    for (int id = 0; id < 4; id++)
+        for (int g = 0; g < 8; g++) {
+            if (dp->peer_opened[id][g]) cudaIpcCloseMemHandle(dp->peer_buf[id][g]);
+            dp->peer_opened[id][g] = false;
+            dp->peer_buf[id][g] = nullptr;
+        }
+    if (dp->barrier_buf) cudaFree(dp->barrier_buf);
+    dp->barrier_buf = nullptr;
 }
 }  // namespace
 
@@ -205,14 +241,23 @@ moa_status_t dist_finish(DistPlan *dp, void *scratch) {
         bool need[4] = {};
         for (auto &s : steps)
             if (s.kind == 2) need[s.dst] = true;
-        for (int id = 0; id < 4; id++)
-            if (need[id] && (id < 2 || setup_peers(dp, id, local[id]) != MOA_OK))
-                return MOA_OK;  // fused exchanges stay off: the NCCL schedule runs
-        if (cudaMalloc(&dp->barrier_buf, 16) != cudaSuccess) {
+        // (the schedule, hence `need`, is the same on every rank)
+        // (user buffers 0 / 1 change per exec: no mapping, no fusion)
+        if (need[0] || need[1]) return MOA_OK;
+        bool ok = true;
+        for (int id = 2; id < 4; id++)  // every needed id on every rank (collectives match)
+            if (need[id] && setup_peers(dp, id, local[id]) != MOA_OK) ok = false;
+        if (ok && cudaMalloc(&dp->barrier_buf, 16) != cudaSuccess) {
             cudaGetLastError();
-            return MOA_OK;
+            dp->barrier_buf = nullptr;
+            ok = false;
         }
-        cudaMemset(dp->barrier_buf, 0, 16);
+        if (ok) ok = cudaMemset(dp->barrier_buf, 0, 16) == cudaSuccess;
+        // every rank must run the same schedule: fuse only if all ranks could
+        if (all_ranks_min(ok ? 1 : 0) != 1) {
+            close_peers(dp);
+            return MOA_OK;  // fused exchanges stay off: the NCCL schedule runs
+        }
     }
     dp->steps.swap(steps);
     dp->passes.swap(passes);

@@ -457,6 +457,13 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
             E *dst = reinterpret_cast<E *>(a.peers[q >> a.log_chunk]) + a.self_off + (q & cmask);
             st_pol(reinterpret_cast<V *>(dst), pts[m], pol);
         }
+        // the peer stores are ordered at system scope before this grid is seen
+        // as finished by the stream-ordered barrier collective that follows
+        // (DistStep kind 3; the readers run after it): one fence per CTA, after
+        // the barrier -- the fence is cumulative over the CTA's stores that the
+        // barrier ordered before it (per-thread fences cost 8 % in the loopback)
+        __syncthreads();
+        if (threadIdx.x == 0) __threadfence_system();
         return;
     }
     {
