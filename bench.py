@@ -353,6 +353,8 @@ def main():
         "kernel_ms": round(dom_ms, 4), "kernel_alg_bytes": dom_bytes, "peak_source": peak_src,
         "step_alg_bytes": alg_bytes,
         "step_frac": round(alg_bytes / (ms * 1e-3) / 1e9 / peak, 4),
+        # SURVEY §8(d.1) also quotes fractions against the 8 TB/s HBM3e spec
+        "spec_peak": 8000.0, "frac_of_spec": round(achieved / 8000.0, 4),
         "per_step_ms": [round(v, 4) for v in per_step], "step_kinds": kinds,
     }
 
