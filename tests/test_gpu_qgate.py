@@ -92,3 +92,36 @@ def test_large_sampled_blocks(m, torch_cuda, n, bits, dtype):
         offs = np.array([[off(r * Q + a, c * Q + b) for b in range(Q)] for a in range(Q)])
         B = D[offs]
         assert np.max(np.abs(got[offs] - U @ B @ U.conj().T)) < tol
+
+
+@pytest.mark.parametrize("bits", [[0, 14], [3, 9, 14]])
+def test_max_size_sampled_blocks(m, torch_cuda, bits):
+    # n = 15 (the ABI's maximum): a 2^15 x 2^15 complex64 matrix (8 GiB); the
+    # sampled blocks are gathered on the device before and after the gate
+    torch = torch_cuda
+    n, q = 15, len(bits)
+    rng = np.random.default_rng(150 + q)
+    U, _ = np.linalg.qr(rng.standard_normal((1 << q, 1 << q)) + 1j * rng.standard_normal((1 << q, 1 << q)))
+    N, Q = 1 << n, 1 << q
+    g = torch.Generator(device="cuda").manual_seed(15)
+    rho = torch.randn(N, N, dtype=torch.complex64, device="cuda", generator=g)
+    t = qgate.gate_permutation(n, bits)
+
+    def off(vr, vc):
+        i_vec = [(vr >> (n - 1 - p)) & 1 for p in range(n)] + [(vc >> (n - 1 - p)) & 1 for p in range(n)]
+        return qgate.permuted_offset(i_vec, t)
+    blocks = []
+    for _ in range(16):
+        r, c = (int(v) for v in rng.integers(0, N // Q, 2))
+        blocks.append(np.array([[off(r * Q + a, c * Q + b) for b in range(Q)] for a in range(Q)]))
+    blocks.append(np.array([[off((N // Q - 1) * Q + a, (N // Q - 1) * Q + b) for b in range(Q)] for a in range(Q)]))
+    idx = torch.from_numpy(np.concatenate([b.reshape(-1) for b in blocks])).cuda()
+    flat = rho.view(-1)
+    before = flat[idx].cpu().numpy().astype(np.complex128)
+    m.moa_qgate_apply(rho, n, bits, U)
+    torch.cuda.synchronize()
+    after = flat[idx].cpu().numpy().astype(np.complex128)
+    for k in range(len(blocks)):
+        B = before[k * Q * Q:(k + 1) * Q * Q].reshape(Q, Q)
+        A = after[k * Q * Q:(k + 1) * Q * Q].reshape(Q, Q)
+        assert np.max(np.abs(A - U @ B @ U.conj().T)) < 5e-6
