@@ -405,22 +405,28 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         if constexpr (!kEarlyTw) fetch_tw();
         double2 w = cmul(tq[0][0], tq[0][1]);
         const double2 ws = cmul(tq[0][2], tq[0][3]);
-        if constexpr (std::is_same<V, float2>::value) {
-            // complex64: the chain in fp32 from fp64-exact endpoints (<= 15
-            // products, ~1e-6 relative against a 2e-5 tolerance) -- no fp64
-            // multiplies or conversions per point
-            float2 wf = cvt_tw(w, V{});
-            const float2 wsf = cvt_tw(ws, V{});
+        if constexpr (LPL == 1) {
+            // w ws^m for m = PB a + b as A[a] B[b] with A[a] = w (ws^PB)^a and
+            // B[b] = ws^b: a dependent depth of ~PA + 2 products instead of the
+            // P - 1 of a plain chain (measured: the chain's latency was 8 % of
+            // cfg2's first pass).  complex64 runs it in fp32 from the fp64-exact
+            // endpoints (<= 6 products per weight, ~1e-6 against 2e-5); complex128
+            // in fp64 (~1e-15)
+            using W = typename std::conditional<std::is_same<V, float2>::value, float2, double2>::type;
+            constexpr int PB = P < 4 ? P : 4, PA = P / PB;
+            const W w0 = cvt_tw(w, W{}), s1 = cvt_tw(ws, W{});
+            W B[PB];
+            B[0] = mk<W>(1, 0);
+            if constexpr (PB > 1) B[1] = s1;
+            if constexpr (PB > 2) B[2] = cmul(s1, s1);
+            if constexpr (PB > 3) B[3] = cmul(B[2], s1);
+            const W sPB = PB > 3 ? cmul(B[2], B[2]) : (PB > 1 ? cmul(B[PB - 1], s1) : s1);
+            W A = w0;
 #pragma unroll
-            for (int m = 0; m < P; m++) {
-                pts[m] = cmul(pts[m], wf);
-                if (m + 1 < P) wf = cmul(wf, wsf);
-            }
-        } else if constexpr (LPL == 1) {
+            for (int ai = 0; ai < PA; ai++) {
 #pragma unroll
-            for (int m = 0; m < P; m++) {
-                pts[m] = cmul(pts[m], cvt_tw(w, V{}));
-                if (m + 1 < P) w = cmul(w, ws);
+                for (int b = 0; b < PB; b++) pts[ai * PB + b] = cmul(pts[ai * PB + b], b ? cmul(A, B[b]) : A);
+                if (ai + 1 < PA) A = cmul(A, sPB);
             }
         } else {  // the pair: the second line's chain
             double2 w1 = cmul(tq[1][0], tq[1][1]);
