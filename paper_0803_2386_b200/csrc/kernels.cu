@@ -240,7 +240,30 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
         V v[Q];
 #pragma unroll
         for (int r = 0; r < Q; r++) v[r] = pts[u + r * G];
-        if constexpr (NS > 1) {
+        if constexpr (NS > 1 && Q >= 4 && std::is_same<V, double2>::value) {
+            // complex128 step twiddles w^r, w = w_{NS Q}^{jm}: one table load (entry
+            // NS + jm - 1 of the step-major table) and the powers as products A[a] B[b]
+            // (r = 4a + b, B[b] = w^b, A[a] = w^{4a}; <= 5 factors deep, ~1e-15) --
+            // measured: the 15 loads per group were ~1/5 of the L1 data-pipe traffic of
+            // the 1024-point passes (3-D passes 6.9 -> 6.5-6.8 ms).  complex64 keeps
+            // the table loads (its passes are issue-bound; the products cost more)
+            using E = typename ElemOf<V>::type;
+            const int jm = j & (NS - 1);
+            const E w1 = __ldg(twR + (NS + jm - 1));
+            const E w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
+            const E B[4] = {w1, w1, w2, w3};  // B[0] unused
+            E A = w4;
+#pragma unroll
+            for (int a = 0; a < Q / 4; a++) {
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int r = 4 * a + b;
+                    if (r == 0) continue;
+                    v[r] = cmul(v[r], a == 0 ? B[b] : (b == 0 ? A : cmul(A, B[b])));
+                }
+                if (a > 0 && a + 1 < Q / 4) A = cmul(A, w4);
+            }
+        } else if constexpr (NS > 1) {
             const int jm = j & (NS - 1);
 #pragma unroll
             // step twiddle w_{NS Q}^{jm r} from the step-major table (entry r NS + jm - 1):

@@ -2,7 +2,7 @@
 """Split a pass's time into access pattern and arithmetic: each descriptor of
 a plan timed as the full pass (moa_fft_exec per-pass events) and as a pure
 movement with the same ONF maps (moa_pass_move: DFT and weights off).
-  move_vs_pass.py n batch dtype"""
+  move_vs_pass.py n batch dtype  |  move_vs_pass.py 3d n0 n1 n2 dtype"""
 import json
 import os
 import sys
@@ -12,12 +12,18 @@ import torch  # noqa: E402
 
 import paper_0803_2386_b200 as m  # noqa: E402
 
-n, B, dt = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+if sys.argv[1] == "3d":
+    shape = tuple(int(v) for v in sys.argv[2:5])
+    dt = sys.argv[5]
+    n, B = shape[0] * shape[1] * shape[2], 1
+    plan = m.FFTPlan.plan_3d(*shape, dtype=dt)
+else:
+    n, B, dt = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    plan = m.FFTPlan(n, B, dt)
 tdt = torch.complex128 if dt == "c128" else torch.complex64
 x = torch.randn(n * B, dtype=tdt, device="cuda")
 y = torch.empty_like(x)
 s = torch.cuda.current_stream()
-plan = m.FFTPlan(n, B, dt)
 for _ in range(3):
     plan.exec(x, y)
 reps = 10
