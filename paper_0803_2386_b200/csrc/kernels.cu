@@ -28,6 +28,9 @@
 
 #include <array>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <utility>
 
@@ -831,16 +834,32 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     // lines per lane -- half the threads and memory instructions per tile
     // (measured: 3-D c64 y-pass 5.12 -> 4.04 ms; slower for <= 2^8-point lines)
     if constexpr (std::is_same<V, float2>::value) {
-        const char *pe = std::getenv("MOA_FFT_C64PAIR");
-        const int min_lr = pe && pe[0] == '1' ? 4 : 10;
-        if (!(pe && pe[0] == '0') && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
+        // MOA_FFT_C64PAIR (ablation): 0 off, 1 also for short lines; read once
+        static const int pair_mode = [] {
+            const char *pe = std::getenv("MOA_FFT_C64PAIR");
+            return pe && pe[0] == '0' ? 0 : pe && pe[0] == '1' ? 2 : 1;
+        }();
+        const int min_lr = pair_mode == 2 ? 4 : 10;
+        if (pair_mode && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
             d.in_str[0] == 1 && d.out_str[0] == 1 && d.W >= 2 && d.logR >= min_lr && d.out_ksplit >= d.logR) {
             KArgs b = a;
             b.W = d.W / 2;
             b.lW = log2_exact(b.W);
             // the pair tile's own shared-memory line stride: 16-byte elements,
-            // W / 2 lines (the descriptor's was chosen for 8-byte elements)
+            // W / 2 lines (the descriptor's was chosen for 8-byte elements);
+            // memoised per tile shape (the bank model is host work per launch)
+            static std::mutex ls_mu;
+            static std::map<std::tuple<int, int, int, int, int>, int32_t> ls_memo;
+            const auto key = std::make_tuple(int(d.logR), int(b.W), int(d.lf_load), int(d.lf_store), int(d.smem_bytes));
+            int32_t memo_ls = -1;
             {
+                std::lock_guard<std::mutex> g(ls_mu);
+                auto it = ls_memo.find(key);
+                if (it != ls_memo.end()) memo_ls = it->second;
+            }
+            if (memo_ls >= 0) {
+                b.LS = memo_ls;
+            } else {
                 const int64_t R = int64_t(1) << d.logR, base = R + R / 16;
                 int64_t best = base, bw = 1 << 30, bt = int64_t(1) << 62;
                 for (int64_t LS = base; LS < base + 16 && (b.W * LS * 16 <= d.smem_bytes); LS++) {
@@ -853,6 +872,8 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                     }
                 }
                 b.LS = int32_t(best);
+                std::lock_guard<std::mutex> g(ls_mu);
+                ls_memo[key] = b.LS;
             }
             KFn<float4> f = kTabPair64[d.logR];
             if (d.smem_bytes > 48 * 1024) {

@@ -263,7 +263,8 @@ moa_status_t qgate_launch(V *rho, int n, uint32_t gmask, int q, const V *u, cuda
     a.RG = int32_t(rgp);
     const int64_t blocks = (rows_groups / rgp) * (a.N / a.TC);
     a.TP = qgate_row_stride(Q, a.TC, a.rdep, a.gpos_dep, int(sizeof(V)));
-    if (const char *e = std::getenv("MOA_QG_TP_OFF")) a.TP = a.TC + std::atoi(e);  // ablation knob
+    static const char *tp_off = std::getenv("MOA_QG_TP_OFF");  // ablation knob, read once
+    if (tp_off) a.TP = a.TC + std::atoi(tp_off);
     const size_t smem = size_t(2) * Q * a.TP * sizeof(V);
     if (blocks > 0x7fffffff) return fail(MOA_EUNSUPPORTED, "qgate: grid too large");
     switch (Q) {
