@@ -155,7 +155,7 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
             // w_{NS Q}^{jm r} (1 <= r < Q, jm < NS) at entry r NS + jm - 1; the
             // steps tile [0, R - 1) exactly (sum_s (Q_s - 1) NS_s = R - 1)
             const int64_t R = int64_t(1) << d.logR;
-            const int LP = d.logR < 4 ? d.logR : 4;
+            const int LP = psi_log_p(d.logR, p->dtype);
             const int nstep = d.logR == 0 ? 1 : (d.logR + LP - 1) / LP;
             std::vector<long double> v(2 * (R > 1 ? R - 1 : 1), 0.0L);
             for (int st = 1; st < nstep; st++) {

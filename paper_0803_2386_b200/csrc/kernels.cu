@@ -108,10 +108,28 @@ template <int LQ> __device__ __forceinline__ constexpr int brev(int k) {
         if (k & (1 << b)) r |= 1 << (LQ - 1 - b);
     return r;
 }
+// z * w_32^e for a compile-time e in [0, 16): even e is w_16^{e/2}; odd e a
+// general multiply by the constant (the radix-32 steps only)
+template <int E, typename V> __device__ __forceinline__ V rot32(V z) {
+    if constexpr (E % 2 == 0) {
+        return rot16<E / 2>(z);
+    } else {
+        using T = typename RealOf<V>::type;
+        constexpr double A = 0.98078528040323044913, B = 0.19509032201612826785;  // cos, sin(pi/16)
+        constexpr double C = 0.83146961230254523708, D = 0.55557023301960222474;  // cos, sin(3 pi/16)
+        constexpr double c = E == 1 ? A : E == 3 ? C : E == 5 ? D : E == 7 ? B : E == 9 ? -B : E == 11 ? -D
+                                                                                           : E == 13 ? -C : -A;
+        constexpr double s = E == 1 ? B : E == 3 ? D : E == 5 ? C : E == 7 ? A : E == 9 ? A : E == 11 ? C
+                                                                                          : E == 13 ? D : B;
+        return cmul(z, mk<V>(T(c), T(-s)));  // w_32^e = cos(pi e/16) - i sin(pi e/16)
+    }
+}
 template <int LQ, int H, int G, int I, typename V> __device__ __forceinline__ void dif_bfly(V *v) {
     V a = v[G + I], b = v[G + I + H];
     v[G + I] = cadd(a, b);
-    v[G + I + H] = rot16<I *(8 / H)>(csub(a, b));
+    // (a - b) w_{2H}^I
+    if constexpr (H == 16) v[G + I + H] = rot32<I>(csub(a, b));
+    else v[G + I + H] = rot16<I *(8 / H)>(csub(a, b));
 }
 template <int LQ, int H, typename V, int... Is> __device__ __forceinline__ void dif_span(V *v, std::integer_sequence<int, Is...>) {
     // Is enumerates (group, i) pairs: g = (idx / H) * 2H, i = idx % H
@@ -140,8 +158,14 @@ template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
 // bank-conflict free, and every (base + compile-time offset) folds into the
 // instruction's immediate (no per-access swizzle arithmetic).  The line stride
 // LS is chosen on the host by a conflict model of all the patterns
-// (psi_choose_tile).  LB is unused (kept for the template signature).
-template <int LB> __device__ __forceinline__ int swz(int i) { return i + (i >> 4); }
+// (psi_choose_tile).  LB is log2 of the pad period: one pad element per 2^LB
+// (16; 32 for the radix-32 steps of complex128 1024-point lines, whose step-0
+// writes are 32 elements apart -- psi_pad_shift on the host).
+template <int LB> __device__ __forceinline__ int swz(int i) { return i + (i >> LB); }
+// log2 of the points per thread (psi_log_p on the host)
+template <typename V, int LR> __host__ __device__ constexpr int lp_of() {
+    return (std::is_same<V, double2>::value && LR == 10) ? 5 : (LR < 4 ? LR : 4);
+}
 
 struct KArgs {
     const void *in;
@@ -343,12 +367,12 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
 // pair_kernel); the ring side's address gets slot * ringG added.
 template <typename V, int LR>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
-                                             V (&pts)[1 << (LR < 4 ? LR : 4)], int64_t b_io, int64_t b_oo,
+                                             V (&pts)[1 << lp_of<V, LR>()], int64_t b_io, int64_t b_oo,
                                              int64_t b_te) {
     (void)line0;
-    constexpr int LP = LR < 4 ? LR : 4;
+    constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
-    constexpr int LB = sizeof(V) == 16 ? 3 : 4;  // log2(elements per 128-byte row)
+    constexpr int LB = LP == 5 ? 5 : 4;  // shared-memory pad period (log2)
     constexpr int NSTEP = LR == 0 ? 1 : (LR + LP - 1) / LP;
     using E = typename ElemOf<V>::type;
     constexpr int LPL = lines_per_lane<V>();  // lines per lane (2: paired complex64)
@@ -518,7 +542,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
 // One tile with direct (register) loads -- the non-pipelined form.
 template <typename V, int LR>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
-    constexpr int LP = LR < 4 ? LR : 4;
+    constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     using E = typename ElemOf<V>::type;
     constexpr int LPL = lines_per_lane<V>();
@@ -552,7 +576,9 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
 }
 
 template <typename V, int LR>
-__global__ void __launch_bounds__(512) pass_kernel(const KArgs a) {
+// (radix-32 kernels: at most 256 threads, so 255 registers -- a cap of 168 for
+// three CTAs per SM spills and measured slower, profiles/r1_s7_radix32.txt)
+__global__ void __launch_bounds__(lp_of<V, LR>() == 5 ? 256 : 512) pass_kernel(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }
@@ -610,7 +636,7 @@ __device__ __forceinline__ void decode_tile(const PairArgs &p, int64_t pos, bool
 // fetching its next tile index while it works on the current one, so the
 // queue atomic's latency is hidden.
 template <typename V, int LRA, int LRB>
-__global__ void __launch_bounds__(512) pair_kernel(const __grid_constant__ PairArgs p) {
+__global__ void __launch_bounds__((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5) ? 256 : 512) pair_kernel(const __grid_constant__ PairArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t total = p.groups * (p.TA + p.TB);
     // the per-group completion counters only ever grow, by exactly TA / TB per launch

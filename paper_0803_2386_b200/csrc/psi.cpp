@@ -54,12 +54,12 @@ static void add_digit(moa_pass_desc_t &d, int64_t ext, int64_t is, int64_t os, i
 }
 
 static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W);
-int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total);
+int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total, int logP);
 
 void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     const int esize = dtype == MOA_C128 ? 16 : 8;
     const int slots = 128 / esize;        // elements per 128-byte smem row / DRAM line
-    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int logR = d.logR, logP = psi_log_p(logR, dtype);
     const int64_t R = int64_t(1) << logR, TPL = R >> logP;
     const bool lf = d.lf_load || d.lf_store;
     const int64_t ext0 = d.ndig ? d.ext[0] : 1;
@@ -88,7 +88,8 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
     const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
     if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
-    while (W > 1 && (W * R * esize > smem_cap || W * TPL > 512 || ext0 % W)) W >>= 1;
+    const int64_t max_thr = logP == 5 ? 256 : 512;  // the radix-32 kernels keep 255 registers
+    while (W > 1 && (W * R * esize > smem_cap || W * TPL > max_thr || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
 }
@@ -96,16 +97,16 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
 // a legal tile of exactly W lines? (used to give both passes of a fused pair the same CTA size)
 static bool tile_ok(const moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
     const int esize = dtype == MOA_C128 ? 16 : 8;
-    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int logR = d.logR, logP = psi_log_p(logR, dtype);
     const int64_t R = int64_t(1) << logR, TPL = R >> logP;
     const int64_t ext0 = d.ndig ? d.ext[0] : 1;
-    return W >= 1 && W * TPL <= 512 && W * R * esize <= 100 * 1024 && ext0 % W == 0;
+    return W >= 1 && W * TPL <= (logP == 5 ? 256 : 512) && W * R * esize <= 100 * 1024 && ext0 % W == 0;
 }
 
 static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
     const int esize = dtype == MOA_C128 ? 16 : 8;
     const int slots = 128 / esize;
-    const int logR = d.logR, logP = logR < 4 ? logR : 4;
+    const int logR = d.logR, logP = psi_log_p(logR, dtype);
     const int64_t R = int64_t(1) << logR, TPL = R >> logP;
     const bool lf = d.lf_load || d.lf_store;
     d.W = int32_t(W);
@@ -115,11 +116,11 @@ static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
     // every access pattern of this tile (exchange writes/reads of each step in
     // its thread mapping), evaluated exactly on the first warps
     (void)slots;
-    const int64_t base = R + R / 16;
+    const int64_t base = R + (R >> psi_pad_shift(logP));
     int64_t best = base, best_w = 1 << 30, best_t = int64_t(1) << 62;
     for (int64_t LS = base; LS < base + 2 * (128 / esize); LS++) {
         int64_t tot = 0;
-        const int w = psi_bank_conflicts(logR, W, esize, d.lf_load, d.lf_store, LS, &tot);
+        const int w = psi_bank_conflicts(logR, W, esize, d.lf_load, d.lf_store, LS, &tot, logP);
         if (w < best_w || (w == best_w && tot < best_t)) {
             best = LS;
             best_w = w;
@@ -137,13 +138,14 @@ static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
 // element (j/NS) NS Q + j%NS + r NS; the next step reads t + m R/P.  Thread
 // mapping: step 0 in the load side's, later steps in the store side's
 // (line-fast: l = tid % W, t = tid / W; point-fast: l = tid / TPL, t = tid % TPL).
-int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total) {
-    const int logP = logR < 4 ? logR : 4;
+int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total, int logP) {
+    if (logP < 0) logP = logR < 4 ? logR : 4;
+    const int sh = psi_pad_shift(logP);
     const int64_t R = int64_t(1) << logR, P = int64_t(1) << logP, TPL = R / P, nthr = W * TPL;
     const int per = 128 / esize;  // lanes per shared-memory wavefront
     const int nstep = logR == 0 ? 1 : (logR + logP - 1) / logP;
     const int lql = logR - logP * (nstep - 1);
-    auto phys = [](int64_t i) { return i + (i >> 4); };
+    auto phys = [sh](int64_t i) { return i + (i >> sh); };
     auto map = [&](int64_t tid, bool lf, int64_t &l, int64_t &t) {
         if (lf) { l = tid % W; t = tid / W; }
         else { l = tid / TPL; t = tid % TPL; }
