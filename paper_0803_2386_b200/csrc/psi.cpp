@@ -75,6 +75,11 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // complex128 strided passes of <= 2^8 points: 256-byte runs (16 lines) --
     // measured cfg3 5.50 -> 5.24 ms (the 32 MiB-stride first pass 1.50 -> 1.33 ms)
     if (lf && esize == 16 && logR >= 5 && logR <= 8) W = 2 * slots;
+    // complex64 strided loads >= 1 MiB apart (cfg4's first pass: 32 MiB): 256-byte
+    // runs too (32 lines) -- measured: its movement time 3.19 -> 2.60 ms, the pass
+    // 3.48 -> 3.33 ms; passes with shorter strides keep 16 lines (no gain there)
+    if (lf && esize == 8 && d.lf_load && d.in_kstr * esize >= (int64_t(1) << 20) && logR >= 5 && logR <= 8)
+        W = 4 * slots;
     // two CTAs per SM by default; MOA_FFT_SMEM_CAP (bytes) overrides (ablations)
     // A line-coalesced side whose points are >= 1 MiB apart (the 3-D x-pass:
     // 16 MiB) touches one DRAM page per point: give it full 128-byte runs even at
