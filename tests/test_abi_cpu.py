@@ -78,6 +78,23 @@ def test_planner_liftings():
         assert int(np.prod(r)) == 1 << t and all(x <= 4096 for x in r)
 
 
+def test_bench_config_tiles():
+    # the tile shapes the measurements chose (profiles/r1_s7_*):
+    # cfg2 two 256-point passes, 16-line tiles (256-byte runs)
+    d2 = m.moa_psi_describe(1 << 16, 1024, "c128")
+    assert [(1 << d["logR"], d["W"], d["threads"]) for d in d2] == [(256, 16, 256), (256, 16, 256)]
+    # cfg4: the first pass loads 32 MiB apart -> 32 lines (256-byte runs of complex64)
+    d4 = m.moa_psi_describe(1 << 30, 1, "c64")
+    assert [1 << d["logR"] for d in d4] == [256, 128, 128, 256]
+    assert d4[0]["W"] == 32 and d4[0]["threads"] == 512 and d4[1]["W"] == 16
+    # cfg5: complex128 1024-point lines take 32 points per thread (radix 32 x 32)
+    for d in m.moa_psi_describe_3d(1024, 1024, 1024, "c128"):
+        assert d["logR"] == 10 and d["W"] * 32 == d["threads"] and d["threads"] <= 256
+    # complex64 1024-point lines keep 16 points per thread
+    for d in m.moa_psi_describe_3d(64, 64, 1024, "c64")[:1]:
+        assert d["logR"] == 10 and d["threads"] == d["W"] * 64
+
+
 def _as_dict(load, store, tw):
     return {tuple(a): (tuple(b), tuple(c)) for a, b, c in zip(load.tolist(), store.tolist(), tw.tolist())}
 
