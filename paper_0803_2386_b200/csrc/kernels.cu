@@ -164,7 +164,7 @@ template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
 template <int LB> __device__ __forceinline__ int swz(int i) { return i + (i >> LB); }
 // log2 of the points per thread (psi_log_p on the host)
 template <typename V, int LR> __host__ __device__ constexpr int lp_of() {
-    return (std::is_same<V, double2>::value && LR == 10) ? 5 : (LR < 4 ? LR : 4);
+    return (std::is_same<V, double2>::value && (LR == 10 || LR == 9)) ? 5 : (LR < 4 ? LR : 4);
 }
 
 struct KArgs {

@@ -87,7 +87,7 @@ def test_bench_config_tiles():
     d4 = m.moa_psi_describe(1 << 30, 1, "c64")
     assert [1 << d["logR"] for d in d4] == [256, 128, 128, 256]
     assert d4[0]["W"] == 32 and d4[0]["threads"] == 512 and d4[1]["W"] == 16
-    # cfg5: complex128 1024-point lines take 32 points per thread (radix 32 x 32)
+    # cfg5: complex128 1024-point lines take 32 points per thread (radix 32 x 32; 512-point lines too)
     for d in m.moa_psi_describe_3d(1024, 1024, 1024, "c128"):
         assert d["logR"] == 10 and d["W"] * 32 == d["threads"] and d["threads"] <= 256
     # complex64 1024-point lines keep 16 points per thread
