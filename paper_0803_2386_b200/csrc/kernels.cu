@@ -164,7 +164,8 @@ template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
 template <int LB> __device__ __forceinline__ int swz(int i) { return i + (i >> LB); }
 // log2 of the points per thread (psi_log_p on the host)
 template <typename V, int LR> __host__ __device__ constexpr int lp_of() {
-    return (std::is_same<V, double2>::value && (LR == 10 || LR == 9)) ? 5 : (LR < 4 ? LR : 4);
+    return ((std::is_same<V, double2>::value || std::is_same<V, float2>::value) && (LR == 9 || LR == 10)) ? 5
+                                                                                            : (LR < 4 ? LR : 4);
 }
 
 struct KArgs {
@@ -866,7 +867,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             return pe && pe[0] == '0' ? 0 : pe && pe[0] == '1' ? 2 : 1;
         }();
         const int min_lr = pair_mode == 2 ? 4 : 10;
-        if (pair_mode && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
+        if (pair_mode && psi_log_p(d.logR, MOA_C64) == 4 && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
             d.in_str[0] == 1 && d.out_str[0] == 1 && d.W >= 2 && d.logR >= min_lr && d.out_ksplit >= d.logR) {
             KArgs b = a;
             b.W = d.W / 2;

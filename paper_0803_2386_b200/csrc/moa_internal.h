@@ -35,12 +35,13 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
 void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype);
 // worst conflict degree (and total extra wavefronts) of a tile's exchange patterns
 int psi_bank_conflicts(int logR, int64_t W, int esize, int lfA, int lfB, int64_t LS, int64_t *total, int logP = -1);
-// Points per thread of a pass (log2): 16, except complex128 512- and 1024-point
-// lines, which take 32 (radix 32 x 16 / 32 x 32: one shared-memory exchange
-// instead of two);
+// Points per thread of a pass (log2): 16, except 512- and 1024-point lines,
+// which take 32 (radix 32 x 16 / 32 x 32: one shared-memory exchange instead
+// of two; the paired-complex64 kernel keeps 16 and is used only where this is 4);
 // the shared-memory line pads one element per 2^psi_pad_shift elements.
 inline int psi_log_p(int logR, moa_dtype_t dtype) {
-    return (dtype == MOA_C128 && (logR == 10 || logR == 9)) ? 5 : (logR < 4 ? logR : 4);
+    (void)dtype;
+    return (logR == 9 || logR == 10) ? 5 : (logR < 4 ? logR : 4);
 }
 inline int psi_pad_shift(int logP) { return logP == 5 ? 5 : 4; }
 

@@ -90,9 +90,13 @@ def test_bench_config_tiles():
     # cfg5: complex128 1024-point lines take 32 points per thread (radix 32 x 32; 512-point lines too)
     for d in m.moa_psi_describe_3d(1024, 1024, 1024, "c128"):
         assert d["logR"] == 10 and d["W"] * 32 == d["threads"] and d["threads"] <= 256
-    # complex64 1024-point lines keep 16 points per thread
-    for d in m.moa_psi_describe_3d(64, 64, 1024, "c64")[:1]:
-        assert d["logR"] == 10 and d["threads"] == d["W"] * 64
+    # complex64 1024-point lines too; a contiguous (point-fast both sides)
+    # >= 1024-point line is one CTA of its own
+    d = m.moa_psi_describe_3d(64, 64, 1024, "c64")[0]
+    assert d["logR"] == 10 and d["lf_load"] == 0 and d["lf_store"] == 0 and d["W"] == 1 and d["threads"] == 32
+    # lines of <= 256 points keep 16 points per thread
+    d = m.moa_psi_describe(1 << 16, 4, "c64")[1]
+    assert d["logR"] == 8 and d["threads"] == d["W"] * 16
 
 
 def _as_dict(load, store, tw):
