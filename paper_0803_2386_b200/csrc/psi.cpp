@@ -667,9 +667,13 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
         for (int x : {a, b, b, a}) radices.push_back(int64_t(1) << x);
         return MOA_OK;
     }
-    // P passes: P-1 strided passes of <= max_mid bits plus a last pass <= max_single
+    // P passes: P-1 strided passes of <= max_mid bits plus a last pass <= max_last
+    // (2^11 / 2^10 points: a longer last line needs two exchanges and measured
+    // slower than one more pass -- 2^21 c128 0.297 -> 0.268 ms, 2^22 c64 0.375 ->
+    // 0.281 ms, profiles/r1_s7_last_pass_cap.txt)
+    const int max_last = dtype == MOA_C128 ? 11 : 10;
     int P = 2;
-    while ((P - 1) * max_mid + max_single < t) P++;
+    while ((P - 1) * max_mid + max_last < t) P++;
     // distribute t bits: balanced, with the last pass taking the remainder
     std::vector<int> bits(P, t / P);
     for (int i = 0; i < t % P; i++) bits[P - 1 - i]++;
