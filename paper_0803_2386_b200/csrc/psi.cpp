@@ -662,7 +662,14 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
     // measured 2^30 c64 11.84 -> 11.33 ms, 2^26 c64 0.756 -> 0.714 ms, 2^26 c128
     // 1.35 -> 1.32 ms against (R, R, R', R') (the strided middle passes run
     // closest to the copy roofline with the shorter lines)
-    if (t >= 26 && t % 2 == 0 && t <= 32) {
+    // Since the 512/1024-point lines run radix 32 (one exchange), t = 26 and 28
+    // take three passes instead (general rule below: 2^26 c128 1.31 -> 1.06 ms,
+    // 2^28 c128 5.14 -> 4.94 ms, c64 -10 / -6 %, profiles/r1_s7_three_pass.txt);
+    // t = 30, 32 keep four (2^30 c64: 11.1 vs 13.5 ms with 1024^3).  The opt-in
+    // L2 pairs (MOA_FFT_LIFT4) need the four factors.
+    const char *l4env = std::getenv("MOA_FFT_LIFT4");
+    const bool lift4 = l4env && l4env[0] == '1';
+    if (t >= (lift4 ? 26 : 30) && t % 2 == 0 && t <= 32) {
         const int a = (t + 3) / 4, b = t / 2 - a;
         for (int x : {a, b, b, a}) radices.push_back(int64_t(1) << x);
         return MOA_OK;

@@ -69,7 +69,8 @@ def test_other_argument_errors():
 def test_planner_liftings():
     assert m.moa_plan_radices(1 << 10) == [1 << 10]
     assert m.moa_plan_radices(1 << 16) == [256, 256]
-    assert m.moa_plan_radices(1 << 28, 1, "c128") == [128, 128, 128, 128]    # two fused pairs
+    assert m.moa_plan_radices(1 << 28, 1, "c128") == [512, 512, 1024]        # radix-32 lines: 3 passes
+    assert m.moa_plan_radices(1 << 26, 1, "c64") == [256, 512, 512]
     assert m.moa_plan_radices(1 << 30, 1, "c64") == [256, 128, 128, 256]
     r3 = m.moa_plan_radices(1 << 27, 1, "c128")                              # odd t: three passes
     assert np.prod(r3) == 1 << 27 and len(r3) == 3 and max(r3[:-1]) <= 512
