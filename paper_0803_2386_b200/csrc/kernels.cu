@@ -10,16 +10,19 @@
 //                shared memory; a pass with contiguous lines loads directly into
 //                registers ("point-fast").
 //   2. block butterflies -- the R-point DFT of every line as a sequence of
-//                Stockham steps of radix Q <= 16 done in registers (an in-register
-//                radix-2 network, FMA-shaped), with the step twiddles of a
-//                self-sorting (autosort) schedule.  The paper's input bit reversal
-//                P_n is never materialised: each step's output index map
-//                absorbs it (step a3).  Exchanges between steps go through
-//                shared memory with one pad element per 16 and a line stride
-//                chosen on the host by a bank-conflict model (psi_choose_tile).
+//                Stockham steps of radix Q <= 16 (Q <= 32 for 512- and 1024-point
+//                lines: 32 points per thread, one exchange) done in registers (an
+//                in-register radix-2 network, FMA-shaped), with the step twiddles
+//                of a self-sorting (autosort) schedule.  The paper's input bit
+//                reversal P_n is never materialised: each step's output
+//                index map absorbs it (step a3).  Exchanges between steps go
+//                through shared memory with one pad element per 16 (32) and a line
+//                stride chosen on the host by a bank-conflict model
+//                (psi_choose_tile).
 //   3. twiddle -- the lifted weights w_N^{(j k) mod N} from a
-//                two-level table (exact integer exponent; two table reads and one
-//                complex multiply), fused before the store.
+//                two-level table (exact integer exponent; two lookups per thread,
+//                the thread's 16 / 32 weights as two-level products), fused
+//                before the store.
 //   4. store  -- point-fast, or line-fast through shared memory (the final
 //                transpose F / digit reversal) with 128-byte runs.
 // No tensor cores: the FFT is not a dense contraction.
