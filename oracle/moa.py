@@ -286,3 +286,44 @@ def lift_pass_maps(radices: Sequence[int], batch: int = 1) -> list:
                 tw.append([0] * Rp)
             passes.append(dict(R=Rp, load=load, store=store, tw=tw, twN=1))
     return passes
+
+
+def lift_line_maps(radices: Sequence[int], batch: int, p: int, line: Tuple[int, int]) -> dict:
+    """One line of lift_pass_maps(radices, batch)[p] without materialising the
+    array, so the config liftings (n up to 2^30) can be checked line by line.
+    The same MoA definitions, applied pointwise:
+      * <o k j> psi (s rho-hat iota N) = gamma(<o k j>; s) -- psi of a full index
+        selects the ravel element at its gamma offset (Def. gammadef
+        P:1000-1019), and the ravel of iota is the offset itself;
+      * the last pass's store position of source s is the offset, in the
+        axis-reversing transpose T of <batch R_0 ... R_{P-1}> rho-hat iota, of the
+        element whose value is s: T[q] = z[q'] with q'_a = q_{perm[a]}
+        (transpose() above, Eq. b_vs_a), so s = gamma(q'; shape) and its
+        position is gamma(q; bshape) with q_{perm[a]} = q'_a.
+    line = (o, j): o the rows above axis p, j < S_p (0 for the last pass).
+    -> dict(R, load, store, tw, twN) with one row each."""
+    radices = list(radices)
+    P = len(radices)
+    n = pi(radices)
+    total = batch * n
+    Rp, Sp = radices[p], pi(radices[p + 1:])
+    Bp = total // (Rp * Sp)
+    o, j = line
+    load = [gamma((o, k, j), (Bp, Rp, Sp)) for k in range(Rp)]
+    if p < P - 1:
+        return dict(R=Rp, load=load, store=list(load), tw=[(j * k) % (Rp * Sp) for k in range(Rp)],
+                    twN=Rp * Sp)
+    shape = [batch] + radices
+    d = len(shape)
+    perm = [0] + [P - ax + 1 for ax in range(1, P + 1)]
+    bshape = [0] * d
+    for ax in range(d):
+        bshape[perm[ax]] = shape[ax]
+    store = []
+    for s in load:
+        qp = gamma_inv(s, shape)          # q' : the element's index in z
+        q = [0] * d
+        for ax in range(d):
+            q[perm[ax]] = qp[ax]
+        store.append(gamma(q, bshape))
+    return dict(R=Rp, load=load, store=store, tw=[0] * Rp, twN=1)

@@ -202,8 +202,15 @@ def moa_qgate_apply(rho, n: int, gated_bits, u, stream=None) -> None:
     complex64/complex128); u: the 2^q x 2^q gate (numpy / host)."""
     import numpy as np
     import torch
+    if rho.dtype not in (torch.complex64, torch.complex128) or not rho.is_cuda or not rho.is_contiguous():
+        raise ValueError("qgate: rho must be a contiguous CUDA complex64 / complex128 tensor")
+    if tuple(rho.shape) != (1 << n, 1 << n):
+        raise ValueError(f"qgate: rho must be 2^n x 2^n = {(1 << n, 1 << n)}, got {tuple(rho.shape)}")
     dt = MOA_C128 if rho.dtype == torch.complex128 else MOA_C64
     uh = np.ascontiguousarray(u, dtype=np.complex128 if dt == MOA_C128 else np.complex64)
+    q = len(gated_bits)
+    if uh.shape != (1 << q, 1 << q):
+        raise ValueError(f"qgate: u must be 2^q x 2^q = {(1 << q, 1 << q)} for {q} gated bits, got {uh.shape}")
     bits = (ctypes.c_int32 * len(gated_bits))(*gated_bits)
     s = stream if stream is not None else torch.cuda.current_stream(rho.device)
     _check(lib.moa_qgate_apply(rho.data_ptr(), n, bits, len(gated_bits), uh.ctypes.data, dt, s.cuda_stream))
@@ -387,6 +394,10 @@ class FFTPlan:
             raise ValueError(f"exec: expected {self.local_elems} elements, got {x.numel()}")
         if out is None:
             out = torch.empty_like(x)
+        elif (out.dtype != want or out.device != x.device or not out.is_contiguous()
+              or out.numel() != self.local_elems):
+            raise ValueError(f"exec: out must be a contiguous {want} tensor of {self.local_elems} elements "
+                             f"on {x.device}")
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         moa_fft_exec(self.h, x.data_ptr(), out.data_ptr(), s.cuda_stream)
         return out
@@ -394,6 +405,11 @@ class FFTPlan:
     def exec_host(self, x_host, out_host, stream=None):
         """End-to-end: host (pinned) buffers in and out; synchronises."""
         import torch
+        want = torch.complex64 if self.dtype == MOA_C64 else torch.complex128
+        for name, t in (("x_host", x_host), ("out_host", out_host)):
+            if t.is_cuda or t.dtype != want or not t.is_contiguous() or t.numel() != self.local_elems:
+                raise ValueError(f"exec_host: {name} must be a contiguous host {want} tensor of "
+                                 f"{self.local_elems} elements")
         s = stream if stream is not None else torch.cuda.current_stream()
         moa_fft_exec_host(self.h, x_host.data_ptr(), out_host.data_ptr(), s.cuda_stream)
         return out_host

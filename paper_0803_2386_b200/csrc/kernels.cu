@@ -674,7 +674,9 @@ __global__ void __launch_bounds__((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5)
                 dep = p.cntB + g - (p.slot_mask + 1);
                 need = round * (unsigned long long)p.TB;
             }
-            if (dep && ld_relaxed(dep) < need) {
+            if (dep && ld_relaxed(dep) >= need) {
+                __threadfence();  // acquire: the producers' ring stores happen-before this tile's loads
+            } else if (dep) {
                 if (have_prev) {
                     __threadfence();
                     atomicAdd(prev_B ? p.cntB + prev_g : p.cntA + prev_g, 1ull);
@@ -686,6 +688,9 @@ __global__ void __launch_bounds__((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5)
                     __nanosleep(32);
                     if (++spins > (1u << 26)) __trap();
                 }
+                // acquire side of the producer's fence + atomicAdd (the relaxed polls
+                // alone would not order this CTA's ring loads after the producer's stores)
+                __threadfence();
                 if (p.stats) {  // MOA_FFT_STATS: waits, spins, wait cycles
                     atomicAdd(p.stats + (isB ? 0 : 3), 1ull);
                     atomicAdd(p.stats + (isB ? 1 : 4), (unsigned long long)spins);
@@ -810,7 +815,7 @@ const std::array<KFn<float4>, 13> kTabPair64 = make_table<float4>(std::make_inte
 const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
 
 KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines,
-                const PassMods &mods) {
+                const PassMods &mods, int dtype_esize) {
     KArgs a{};
     a.conj_in = mods.conj_in;
     a.conj_out = mods.conj_out;
@@ -849,7 +854,17 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.lf_load = d.lf_load;
     a.lf_store = d.lf_store;
     a.ring = d.ring;
-    a.discard = d.ring_discard;
+    // discard.global.L2 drops whole 128-byte lines: only when every line a
+    // consumed 128-byte run touches belongs to this tile (a line-fast side with
+    // adjacent lines adjacent in memory and W * esize >= 128, or a point-fast
+    // side with contiguous points and R * esize >= 128) -- otherwise it would
+    // also drop lines the next tile has not read yet
+    {
+        const int64_t esize = dtype_esize;
+        const bool lf_ok = d.lf_load && d.ndig >= 1 && d.in_str[0] == 1 && int64_t(d.W) * esize >= 128;
+        const bool pf_ok = !d.lf_load && d.in_kstr == 1 && (int64_t(1) << d.logR) * esize >= 128;
+        a.discard = d.ring_discard && (lf_ok || pf_ok);
+    }
     return a;
 }
 
@@ -857,7 +872,7 @@ template <typename V>
 cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
                      const DevTables &tb, cudaStream_t stream, const PassMods &mods) {
     int64_t nlines = 0;
-    KArgs a = fill_args(d, in, out, tb, &nlines, mods);
+    KArgs a = fill_args(d, in, out, tb, &nlines, mods, int(sizeof(typename ElemOf<V>::type)));
     const int64_t tiles = nlines / d.W;
     // complex64 passes of >= 2^10-point lines coalesced along the lines on both
     // sides (digit 0 unit stride in and out, even tile width): two adjacent
@@ -929,8 +944,8 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
                           cudaStream_t stream, const PassMods &mA, const PassMods &mB) {
     int64_t nA = 0, nB = 0;
     PairArgs p{};
-    p.A = fill_args(dA, in, rs.ring, tA, &nA, mA);
-    p.B = fill_args(dB, rs.ring, out, tB, &nB, mB);
+    p.A = fill_args(dA, in, rs.ring, tA, &nA, mA, int(sizeof(V)));
+    p.B = fill_args(dB, rs.ring, out, tB, &nB, mB, int(sizeof(V)));
     p.TA = int32_t((nA / dA.W) / dA.ring_groups);
     p.TB = int32_t((nB / dB.W) / dB.ring_groups);
     p.groups = dA.ring_groups;
@@ -940,7 +955,10 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
     p.qctr = rs.qctr;
     p.cntA = rs.cntA;
     p.cntB = rs.cntB;
-    p.epoch = rs.epoch;
+    // the completion counters are reset on the stream before every launch (so a
+    // captured CUDA graph replays correctly: no host-side epoch baked into the
+    // arguments); the kernel waits for counts of exactly TA / TB
+    p.epoch = 0;
     p.stats = rs.stats;
     PFn<V> fn = tab[(dA.logR - 5) * 6 + (dB.logR - 5)];
     const int smem = dA.smem_bytes > dB.smem_bytes ? dA.smem_bytes : dB.smem_bytes;
@@ -957,8 +975,15 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t grid = int64_t(per_sm > 0 ? per_sm : 1) * sms;
     if (grid > tiles) grid = tiles;
-    fn<<<dim3(unsigned(grid)), dim3(unsigned(dA.threads)), size_t(smem), stream>>>(p);
-    return cudaGetLastError();
+    e = cudaMemsetAsync(rs.cntA, 0, size_t(p.groups) * sizeof(unsigned long long), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rs.cntB, 0, size_t(p.groups) * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    // the tile waits need every CTA resident at once: a cooperative launch
+    // fails cleanly (instead of trapping in the watchdog) when the grid cannot
+    // be co-resident, e.g. with other kernels occupying SMs
+    void *kargs[] = {&p};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(unsigned(grid)),
+                                       dim3(unsigned(dA.threads)), kargs, size_t(smem), stream);
 }
 }  // namespace
 

@@ -123,3 +123,27 @@ def run_dist(schedules, shards):
                 for g in range(p):
                     bufs[h][t][g * c:(g + 1) * c] = snap[g][h * c:(h + 1) * c]
     return [b[1] for b in bufs]
+
+
+def enumerate_lines(d, lines):
+    """enumerate_pass restricted to the given ONF line numbers (large passes)."""
+    R = d["R"]
+    rest = np.asarray(lines, dtype=np.int64).copy()
+    io = np.zeros(rest.size, np.int64)
+    oo = np.zeros(rest.size, np.int64)
+    te = np.zeros(rest.size, np.int64)
+    for e, si, so, st in zip(d["ext"], d["in_str"], d["out_str"], d["tw_str"]):
+        dig = rest % e
+        rest //= e
+        io += dig * si
+        oo += dig * so
+        te += dig * st
+    k = np.arange(R, dtype=np.int64)
+    load = io[:, None] + k[None, :] * d["in_kstr"]
+    if d["out_ksplit"] < d["logR"]:
+        koff = (k & ((1 << d["out_ksplit"]) - 1)) * d["out_kstr"] + (k >> d["out_ksplit"]) * d["out_kstr_hi"]
+    else:
+        koff = k * d["out_kstr"]
+    store = oo[:, None] + koff[None, :]
+    tw = ((te[:, None] + d["tw_off"]) * k[None, :]) % d["twN"] if d["twN"] > 1 else np.zeros_like(load)
+    return load, store, tw

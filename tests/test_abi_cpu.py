@@ -12,7 +12,7 @@ import pytest
 import oracle
 import synth
 from oracle import moa
-from onf import enumerate_pass, run_dist, run_plan
+from onf import enumerate_lines, enumerate_pass, run_dist, run_plan
 
 import paper_0803_2386_b200 as m
 
@@ -122,6 +122,39 @@ def test_psi_descriptors_bit_exact_vs_oracle_maps(radices, batch):
         # every element is loaded once and stored once (a permutation per pass)
         assert sorted(load.ravel().tolist()) == list(range(n * batch))
         assert sorted(store.ravel().tolist()) == list(range(n * batch))
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4"])
+def test_psi_descriptors_bit_exact_at_config_liftings(cfg):
+    # the planner's own descriptors at BASELINE.json's full sizes (cfg2 256*256
+    # x 1024 rows, cfg3 2^28, cfg4 2^30 complex64) against the MoA maps of the
+    # same lifting, evaluated pointwise (moa.lift_line_maps) on sampled lines:
+    # the first and last lines and 300 random ones per pass, every point of each
+    c = synth.CONFIGS[cfg]
+    n, batch, dtype = c["n"], c["batch"], c["dtype"]
+    passes = m.moa_psi_describe(n, batch, dtype)
+    radices = [d["R"] for d in passes]
+    assert int(np.prod(radices)) == n
+    rng = np.random.default_rng(11)
+    for p, d in enumerate(passes):
+        assert d["ring"] == 0
+        nlines = int(np.prod(d["ext"]))
+        lines = np.unique(np.concatenate([[0, 1, 2, nlines - 2, nlines - 1], rng.integers(0, nlines, 300)]))
+        load, store, tw = enumerate_lines(d, lines)
+        Sp = int(np.prod(radices[p + 1:]))
+        seen = set()
+        for i in range(lines.size):
+            o, k0, j = moa.gamma_inv(int(load[i, 0]), (batch * n // (d["R"] * Sp), d["R"], Sp))
+            assert k0 == 0
+            ref = moa.lift_line_maps(radices, batch, p, (o, j))
+            assert load[i].tolist() == ref["load"]
+            assert store[i].tolist() == ref["store"]
+            if d["twN"] > 1:
+                assert d["twN"] == ref["twN"] and tw[i].tolist() == ref["tw"]
+            else:
+                assert ref["twN"] == 1 or all(e == 0 for e in ref["tw"])
+            seen.add((o, j))
+        assert len(seen) == lines.size            # distinct ONF lines are distinct MoA lines
 
 
 @pytest.mark.parametrize("n,batch,dtype", [(1 << 12, 2, "c128"), (1 << 16, 1, "c128"), (1 << 13, 1, "c64"),

@@ -222,3 +222,28 @@ def test_lift_maps_are_the_paper_transposes():
                 for a, b in zip(line_l, line_s):
                     out[b] = a
             assert out == moa.final_transpose(list(range(n)), moa.ilog2(c))
+
+
+@pytest.mark.parametrize("radices,batch", [([4, 8], 1), ([8, 8], 2), ([2, 4, 8], 1), ([4, 2, 2, 4], 3),
+                                           ([16], 2), ([8, 4, 16], 1), ([32, 2, 4], 2)])
+def test_lift_line_maps_pointwise(radices, batch):
+    # the pointwise form (gamma / transpose evaluated per element, used for the
+    # config liftings up to 2^30) executes to the DFT on its own, and agrees line
+    # by line with the materialised maps
+    n = moa.pi(radices)
+    P = len(radices)
+    ref_maps = moa.lift_pass_maps(radices, batch)
+    passes = []
+    for p in range(P):
+        Sp = moa.pi(radices[p + 1:])
+        Bp = batch * n // (radices[p] * Sp)
+        rows = [moa.lift_line_maps(radices, batch, p, (o, j)) for o in range(Bp) for j in range(Sp)]
+        ps = dict(R=radices[p], load=[r["load"] for r in rows], store=[r["store"] for r in rows],
+                  tw=[r["tw"] for r in rows], twN=rows[0]["twN"])
+        assert ps["load"] == ref_maps[p]["load"] and ps["store"] == ref_maps[p]["store"]
+        assert ps["tw"] == ref_maps[p]["tw"] and ps["twN"] == ref_maps[p]["twN"]
+        passes.append(ps)
+    x = synth_input(n * batch)
+    got = execute_maps(x, passes)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-13
