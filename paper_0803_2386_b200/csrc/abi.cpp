@@ -475,7 +475,10 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
     const size_t np = p->passes.size();
     NvtxRange exec_range(nvtx_on() ? "moa exec n=" + std::to_string(p->n) : std::string());
     if (p->dist) {
-        st = dist_exec(p->dist, p->passes, p->tabs, p->dtype, in, out, p->scratch, s, evs, p->flags, p->n);
+        std::vector<DistRank> me{{p->dist, &p->passes, &p->tabs,
+                                  {const_cast<void *>(in), out, p->scratch, p->dist->scratch2}, p->flags}};
+        if (p->dist->loopback) return fail(MOA_EINVAL, "exec: a loopback plan runs through moa_fft_exec_loopback");
+        st = dist_exec(me, DistBackend::Nccl, p->dtype, s, evs, p->n);
     } else {
         int step = 0;
         for (size_t i = 0; i < np; i++, step++) {
@@ -761,43 +764,18 @@ extern "C" moa_status_t moa_fft_exec_loopback(moa_fft_plan_t *plans, int ngpu, c
             return fail(MOA_EINVAL, "exec_loopback: plans[r] must be loopback plan of virtual rank r");
         if (!ins[r] || !outs[r]) return fail(MOA_EINVAL, "exec_loopback: null buffer");
     }
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    auto bufs = [&](int r, int id) -> void * {
+    // the product step loop (dist_exec) with the loopback exchange backend
+    std::vector<DistRank> ranks;
+    for (int r = 0; r < ngpu; r++) {
         moa_fft_plan_s *p = plans[r];
-        switch (id) {
-            case 0: return const_cast<void *>(ins[r]);
-            case 1: return outs[r];
-            case 2: return p->scratch;
-            default: return p->dist->scratch2;
-        }
-    };
-    const auto &steps = plans[0]->dist->steps;
-    for (const auto &st : steps) {
-        if (st.kind == 3) continue;  // barrier: the lock-step launch order already provides it
-        if (st.kind == 0 || st.kind == 2) {
-            for (int r = 0; r < ngpu; r++) {
-                const moa_pass_desc_t &d = plans[r]->passes[st.pass];
-                PassMods mods = pass_mods(plans[r]->flags, size_t(st.pass), plans[r]->passes.size(), plans[r]->n);
-                if (st.kind == 2) {  // fused exchange: stores straight into every virtual rank's buffer
-                    mods.npeers = ngpu;
-                    for (int h = 0; h < ngpu; h++) mods.peers[h] = bufs(h, st.dst);
-                    mods.log_chunk = log2_exact(st.count);
-                    mods.self_off = int64_t(r) * st.count;
-                }
-                cudaError_t e = launch_pass(d, plans[r]->dtype, bufs(r, d.src), bufs(r, st.kind == 2 ? st.dst : d.dst),
-                                            plans[r]->tabs[st.pass], s, mods);
-                if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback pass: ") + cudaGetErrorString(e));
-            }
-        } else {
-            const size_t cb = size_t(st.count) * plans[0]->esize;
-            for (int h = 0; h < ngpu; h++)
-                for (int g = 0; g < ngpu; g++) {
-                    char *dst = static_cast<char *>(bufs(h, st.dst)) + size_t(g) * cb;
-                    const char *src = static_cast<const char *>(bufs(g, st.src)) + size_t(h) * cb;
-                    cudaError_t e = cudaMemcpyAsync(dst, src, cb, cudaMemcpyDeviceToDevice, s);
-                    if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback copy: ") + cudaGetErrorString(e));
-                }
-        }
+        ranks.push_back({p->dist, &p->passes, &p->tabs, {const_cast<void *>(ins[r]), outs[r], p->scratch, p->dist->scratch2},
+                         p->flags});
     }
-    return MOA_OK;
+    moa_fft_plan_s *p0 = plans[0];
+    cudaEvent_t *evs = nullptr;
+    if (p0->prof_count < p0->prof_max) evs = &p0->prof_ev[size_t(p0->prof_count) * (p0->prof_nsteps + 1)];
+    moa_status_t st = dist_exec(ranks, DistBackend::Loopback, p0->dtype, reinterpret_cast<cudaStream_t>(stream), evs,
+                                p0->n);
+    if (evs) p0->prof_count++;
+    return st;
 }

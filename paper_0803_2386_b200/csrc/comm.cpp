@@ -425,37 +425,63 @@ int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes) {
     return c;
 }
 
-moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
-                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
-                       cudaEvent_t *evs, uint32_t flags, int64_t N) {
-    if (dp->loopback) return fail(MOA_EINVAL, "dist: a loopback plan runs through moa_fft_exec_loopback");
-    if (!g_comm) return fail(MOA_EINVAL, "dist: no communicator (moa_fft_dist_init)");
-    void *bufs[4] = {const_cast<void *>(in), out, scratch, dp->scratch2};
-    for (size_t i = 0; i < dp->steps.size(); i++) {
-        const DistStep &st = dp->steps[i];
+moa_status_t dist_exec(const std::vector<DistRank> &ranks, DistBackend be, moa_dtype_t dtype, cudaStream_t s,
+                       cudaEvent_t *evs, int64_t N) {
+    if (ranks.empty()) return fail(MOA_EINVAL, "dist: no ranks");
+    const DistPlan *dp0 = ranks[0].dp;
+    const int p = dp0->ngpu;
+    if (be == DistBackend::Nccl) {
+        if (ranks.size() != 1 || dp0->loopback) return fail(MOA_EINVAL, "dist: an NCCL exec runs this process's rank only");
+        if (!g_comm) return fail(MOA_EINVAL, "dist: no communicator (moa_fft_dist_init)");
+    } else if (int(ranks.size()) != p) {
+        return fail(MOA_EINVAL, "dist: a loopback exec runs every virtual rank");
+    }
+    // the peer buffer `id` of rank g as seen by this process: mapped over NVLink
+    // (CUDA IPC, NCCL backend) or the co-located virtual rank's own buffer
+    auto peer = [&](const DistRank &me, int g, int id) -> void * {
+        if (be == DistBackend::Nccl) return me.dp->peer_buf[id][g];
+        return ranks[g].bufs[id];
+    };
+    for (size_t i = 0; i < dp0->steps.size(); i++) {
+        const DistStep &st = dp0->steps[i];  // (every rank runs the same schedule)
         if (evs) cudaEventRecord(evs[i], s);
         if (st.kind == 0 || st.kind == 2) {
-            const moa_pass_desc_t &d = passes[st.pass];
-            PassMods mods = pass_mods(flags, size_t(st.pass), passes.size(), N);
-            if (st.kind == 2) {  // the exchange folded into the stores: NVLink writes into every rank's scratch2
-                mods.npeers = dp->ngpu;
-                for (int g = 0; g < dp->ngpu; g++) mods.peers[g] = dp->peer_buf[st.dst][g];
-                mods.log_chunk = log2_exact(st.count);
-                mods.self_off = int64_t(dp->rank) * st.count;
+            for (const DistRank &r : ranks) {
+                const moa_pass_desc_t &d = (*r.passes)[st.pass];
+                PassMods mods = pass_mods(r.flags, size_t(st.pass), r.passes->size(), N);
+                if (st.kind == 2) {  // the exchange folded into the stores: NVLink writes into every rank's buffer
+                    mods.npeers = p;
+                    for (int g = 0; g < p; g++) mods.peers[g] = peer(r, g, st.dst);
+                    mods.log_chunk = log2_exact(st.count);
+                    mods.self_off = int64_t(r.dp->rank) * st.count;
+                }
+                cudaError_t e = launch_pass(d, dtype, r.bufs[d.src], r.bufs[st.kind == 2 ? st.dst : d.dst],
+                                            (*r.tabs)[st.pass], s, mods);
+                if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("dist pass: ") + cudaGetErrorString(e));
             }
-            cudaError_t e = launch_pass(d, dtype, bufs[d.src], bufs[st.kind == 2 ? st.dst : d.dst], tabs[st.pass], s, mods);
-            if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("dist pass: ") + cudaGetErrorString(e));
         } else if (st.kind == 3) {  // every rank's fused stores have landed before anyone reads them
-            ncclResult_t r = g_nccl.allReduce(dp->barrier_buf, dp->barrier_buf, 1, ncclFloat, ncclSum, g_comm, s);
-            if (r != ncclSuccess) return nccl_fail(r, "barrier");
-        } else {
+            if (be == DistBackend::Nccl) {
+                ncclResult_t rr = g_nccl.allReduce(dp0->barrier_buf, dp0->barrier_buf, 1, ncclFloat, ncclSum, g_comm, s);
+                if (rr != ncclSuccess) return nccl_fail(rr, "barrier");
+            }
+            // loopback: every virtual rank's kernels run in order on one stream
+        } else if (be == DistBackend::Nccl) {
             const size_t cnt = size_t(st.count) * 2;
-            ncclResult_t r = g_nccl.alltoAll(bufs[st.src], bufs[st.dst], cnt, dtype == MOA_C128 ? ncclDouble : ncclFloat,
-                                             g_comm, s);
-            if (r != ncclSuccess) return nccl_fail(r, "all-to-all");
+            ncclResult_t rr = g_nccl.alltoAll(ranks[0].bufs[st.src], ranks[0].bufs[st.dst], cnt,
+                                              dtype == MOA_C128 ? ncclDouble : ncclFloat, g_comm, s);
+            if (rr != ncclSuccess) return nccl_fail(rr, "all-to-all");
+        } else {  // loopback all-to-all: chunk h of rank g -> chunk g of rank h (one copy per chunk)
+            const size_t cb = size_t(st.count) * dp0->esize;
+            for (int h = 0; h < p; h++)
+                for (int g = 0; g < p; g++) {
+                    char *dst = static_cast<char *>(ranks[h].bufs[st.dst]) + size_t(g) * cb;
+                    const char *src = static_cast<const char *>(ranks[g].bufs[st.src]) + size_t(h) * cb;
+                    cudaError_t e = cudaMemcpyAsync(dst, src, cb, cudaMemcpyDeviceToDevice, s);
+                    if (e != cudaSuccess) return fail(MOA_ECUDA, std::string("loopback copy: ") + cudaGetErrorString(e));
+                }
         }
     }
-    if (evs) cudaEventRecord(evs[dp->steps.size()], s);
+    if (evs) cudaEventRecord(evs[dp0->steps.size()], s);
     return MOA_OK;
 }
 

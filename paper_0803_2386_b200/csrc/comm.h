@@ -55,9 +55,25 @@ moa_status_t dist_finish(DistPlan *dp, void *scratch);
 bool dist_ready(int ngpu);
 moa_status_t dist_plan_1d(DistPlan *&dp, int64_t n, moa_dtype_t dtype, bool lifted_order = false);
 moa_status_t dist_plan_3d(DistPlan *&dp, int64_t n0, int64_t n1, int64_t n2, moa_dtype_t dtype);
-moa_status_t dist_exec(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes, const std::vector<DevTables> &tabs,
-                       moa_dtype_t dtype, const void *in, void *out, void *scratch, cudaStream_t s,
-                       cudaEvent_t *evs, uint32_t flags, int64_t N);
+// One rank's view of an exec: its plan, pass descriptors, tables and the four
+// buffers (0 in, 1 out, 2 scratch, 3 scratch2).
+struct DistRank {
+    const DistPlan *dp;
+    const std::vector<moa_pass_desc_t> *passes;
+    const std::vector<DevTables> *tabs;
+    void *bufs[4];
+    uint32_t flags;
+};
+// How the exchanges of the schedule are carried out.  Nccl: this process runs
+// one rank; all-to-alls are ncclAlltoAll, barriers a one-element
+// ncclAllReduce, fused stores go to the CUDA-IPC-mapped peer buffers.
+// Loopback: this process runs every virtual rank on one GPU, in lock step on
+// one stream; all-to-alls are device copies, barriers are stream order, fused
+// stores go to the co-located ranks' buffers.  The step loop, the kernels, the
+// chunk maps and the fused-store routing are the same code for both.
+enum class DistBackend { Nccl, Loopback };
+moa_status_t dist_exec(const std::vector<DistRank> &ranks, DistBackend be, moa_dtype_t dtype, cudaStream_t s,
+                       cudaEvent_t *evs, int64_t N);
 void dist_plan_free(DistPlan *dp);
 int dist_launches(DistPlan *dp, const std::vector<moa_pass_desc_t> &passes);
 

@@ -196,6 +196,11 @@ struct KArgs {
     int32_t log_chunk;
     int64_t self_off;
     void *peers[8];
+    // L2 prefetch ahead (MOA_FFT_PF): at its start a CTA asks the L2 for the
+    // input footprint of tile blockIdx.x + pf_dist (about one wave of resident
+    // CTAs ahead), so that tile's loads hit L2 instead of waiting on DRAM --
+    // the paper's "pre-fetching becomes a deterministic cost"
+    int64_t pf_dist, ntiles;
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -543,6 +548,31 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     }
 }
 
+// Bulk L2 prefetch of `bytes` (multiple of 16) at p (16-byte aligned).
+__device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Prefetch the input footprint of the tile starting at line `line0` into L2:
+// a line-fast side with adjacent lines (one W-line run per point) or a
+// point-fast side with contiguous points (one run per line).
+template <typename V, int LR>
+__device__ __forceinline__ void prefetch_tile(const KArgs &a, int64_t line0) {
+    using E = typename ElemOf<V>::type;
+    constexpr int R = 1 << LR;
+    constexpr int LPL = lines_per_lane<V>();
+    int64_t io, oo, te;
+    line_offsets(a, line0, io, oo, te);
+    const E *in = reinterpret_cast<const E *>(a.in) + io;
+    const int lines = a.W * LPL;
+    if (a.lf_load && a.in_str[0] == 1) {
+        const uint32_t run = uint32_t(lines * int(sizeof(E)));
+        for (int k = threadIdx.x; k < R; k += blockDim.x) l2_prefetch(in + int64_t(k) * a.in_kstr, run);
+    } else if (!a.lf_load && a.in_kstr == 1) {
+        for (int l = threadIdx.x; l < lines; l += blockDim.x) l2_prefetch(in + int64_t(l) * a.in_str[0], uint32_t(R * sizeof(E)));
+    }
+}
+
 // One tile with direct (register) loads -- the non-pipelined form.
 template <typename V, int LR>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
@@ -550,6 +580,10 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     using E = typename ElemOf<V>::type;
     constexpr int LPL = lines_per_lane<V>();
+    if (a.pf_dist) {
+        const int64_t nt = int64_t(blockIdx.x) + a.pf_dist;
+        if (nt < a.ntiles) prefetch_tile<V, LR>(a, nt * a.W * LPL);
+    }
     const TileMap mp = tile_map<TPL>(a);
     int64_t b_io, b_oo, b_te;
     line_offsets(a, line0, b_io, b_oo, b_te);  // the tile's first line; line l adds l * str[0]
@@ -868,12 +902,29 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     return a;
 }
 
+// prefetch distance = f x (CTAs resident on the device at once)
+void set_prefetch(KArgs &a, const void *fn, int threads, int smem, int64_t tiles, double f) {
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    a.pf_dist = int64_t(f * per_sm * sms + 0.5);
+    if (a.pf_dist < 1) a.pf_dist = 1;
+    a.ntiles = tiles;
+}
+
 template <typename V>
 cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
                      const DevTables &tb, cudaStream_t stream, const PassMods &mods) {
     int64_t nlines = 0;
     KArgs a = fill_args(d, in, out, tb, &nlines, mods, int(sizeof(typename ElemOf<V>::type)));
     const int64_t tiles = nlines / d.W;
+    // MOA_FFT_PF = f: prefetch the tile f * (resident CTAs) ahead into L2 (0: off)
+    double pf = 0.0;
+    if (const char *pe = std::getenv("MOA_FFT_PF")) pf = std::atof(pe);
     // complex64 passes of >= 2^10-point lines coalesced along the lines on both
     // sides (digit 0 unit stride in and out, even tile width): two adjacent
     // lines per lane -- half the threads and memory instructions per tile
@@ -925,6 +976,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                 cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
                 if (e != cudaSuccess) return e;
             }
+            if (pf > 0 && !d.ring) set_prefetch(b, reinterpret_cast<const void *>(f), d.threads / 2, d.smem_bytes, tiles, pf);
             f<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads / 2)), size_t(d.smem_bytes), stream>>>(b);
             return cudaGetLastError();
         }
@@ -934,6 +986,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
         if (e != cudaSuccess) return e;
     }
+    if (pf > 0 && !d.ring) set_prefetch(a, reinterpret_cast<const void *>(fn), d.threads, d.smem_bytes, tiles, pf);
     fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
     return cudaGetLastError();
 }
