@@ -143,6 +143,13 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
     std::map<int, const void *> byR;
     std::map<int64_t, std::pair<const void *, const void *>> byN;
     p->tabs.clear();
+    // one tile counter per pass for the warp-specialised kernel (reset on the
+    // exec stream before each of its launches)
+    void *ctrs = nullptr;
+    {
+        moa_status_t st = dev_alloc(p, sizeof(unsigned long long) * (p->passes.size() + 1), &ctrs);
+        if (st) return st;
+    }
     for (auto &d : p->passes) {
         DevTables t;
         auto it = byR.find(d.logR);
@@ -191,6 +198,7 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
                 byN[d.twN] = {t.tw_hi, t.tw_lo};
             }
         }
+        t.ctr = static_cast<unsigned long long *>(ctrs) + p->tabs.size();
         p->tabs.push_back(t);
     }
     return MOA_OK;

@@ -26,10 +26,12 @@
 //   4. store  -- point-fast, or line-fast through shared memory (the final
 //                transpose F / digit reversal) with 128-byte runs.
 // No tensor cores: the FFT is not a dense contraction.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -322,9 +324,27 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
 // tA), every later step in the store mapping (lB, tB): between steps the data
 // passes through shared memory anyway, so the thread <-> line assignment changes
 // for free there and no extra transposition is needed for a strided side.
-template <int LR, int LP, int LB, int S, int NSTEP, typename V>
+// Barrier of the threads that share a tile: the whole CTA (the plain pass
+// kernel), or one consumer warp group of the warp-specialised kernel (a named
+// barrier over its threads).
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {
+    int id, n;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
+// Called once every thread of the tile has read the tile's shared memory for
+// the last time (`synced`: a barrier to that effect has just completed): the
+// warp-specialised kernel hands the stage back to its TMA producer there.
+struct NoFree {
+    __device__ __forceinline__ void operator()(bool) const {}
+};
+
+template <int LR, int LP, int LB, int S, int NSTEP, typename V, typename Sync, typename OnFree>
 __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int lA, int tA, int lB, int tB,
-                                         const typename ElemOf<V>::type *__restrict__ twR) {
+                                         const typename ElemOf<V>::type *__restrict__ twR, const Sync &sync,
+                                         const OnFree &on_free) {
     // radix P for every step but the last, which takes the remainder (so step 0,
     // whose writes are strided by its radix, always has radix 16)
     constexpr int LQL = LR - LP * (NSTEP - 1);
@@ -335,12 +355,13 @@ __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int l
     if constexpr (S == 0) stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lA * LS, tA, twR);
     else stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lB * LS, tB, twR);
     if constexpr (!LAST) {
-        __syncthreads();
+        sync();
         const V *sl = sm + lB * LS;
 #pragma unroll
         for (int m = 0; m < P; m++) pts[m] = sl[swz<LB>(tB + m * (R / P))];
-        __syncthreads();
-        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm, LS, lA, tA, lB, tB, twR);
+        sync();
+        if constexpr (S + 1 == NSTEP - 1) on_free(true);  // no shared-memory access after this
+        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm, LS, lA, tA, lB, tB, twR, sync, on_free);
     }
 }
 
@@ -360,8 +381,7 @@ __device__ __forceinline__ double2 tw_lookup(const double2 *__restrict__ hi, con
 struct TileMap {
     int lA, tA, lB, tB;
 };
-template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
-    const int tid = threadIdx.x;
+template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a, int tid) {
     TileMap m;
     m.lA = a.lf_load ? tid & (a.W - 1) : tid / TPL;
     m.tA = a.lf_load ? tid >> a.lW : tid % TPL;
@@ -374,10 +394,12 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a) {
 // butterflies, lifted weights, store.  ring >= 0: the ring slot of this
 // tile's group (the L2-staged intermediate of a fused pass pair, see
 // pair_kernel); the ring side's address gets slot * ringG added.
-template <typename V, int LR>
+template <typename V, int LR, typename Sync = CtaSync, typename OnFree = NoFree,
+          bool kEarlyTw = std::is_same<V, double2>::value>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
                                              V (&pts)[1 << lp_of<V, LR>()], int64_t b_io, int64_t b_oo,
-                                             int64_t b_te) {
+                                             int64_t b_te, int tid, const Sync &sync = Sync(),
+                                             const OnFree &on_free = OnFree()) {
     (void)line0;
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
@@ -387,7 +409,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     constexpr int LPL = lines_per_lane<V>();  // lines per lane (2: paired complex64)
     E *__restrict__ out = reinterpret_cast<E *>(a.out);
     const E *__restrict__ twR = reinterpret_cast<const E *>(a.twR);
-    const TileMap mp = tile_map<TPL>(a);
+    const TileMap mp = tile_map<TPL>(a, tid);
     const int lA = mp.lA, tA = mp.tA, lB = mp.lB, tB = mp.tB;
 
     // The lifted weights' two-level table entries (step 3 forms their
@@ -396,7 +418,6 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     // (measured cfg3 5.25 -> 5.13 ms, 3-D 19.2 -> 18.8 ms; no occupancy cost at
     // 2 CTAs/SM).  complex64: fetched in step 3 -- holding them costs 9
     // registers and one CTA per SM (64 -> 73; cfg4 11.2 -> 12.0 ms).
-    constexpr bool kEarlyTw = std::is_same<V, double2>::value;
     const int64_t te = b_te + int64_t(LPL * lB) * a.tw_str[0];
     double2 tq[LPL][4];
     auto fetch_tw = [&]() {
@@ -422,7 +443,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     bool moved = false;
     if constexpr (LR > 0 && NSTEP > 1) {
         if (!a.nodft) {
-            line_fft<LR, LP, LB, 0, NSTEP>(pts, sm, a.LS, lA, tA, lB, tB, twR);
+            line_fft<LR, LP, LB, 0, NSTEP>(pts, sm, a.LS, lA, tA, lB, tB, twR, sync, on_free);
             moved = true;
         }
     } else if constexpr (LR > 0) {
@@ -432,17 +453,20 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         V *sl = sm + lA * a.LS;
 #pragma unroll
         for (int m = 0; m < P; m++) sl[swz<LB>(tA + m * TPL)] = pts[m];
-        __syncthreads();
+        sync();
         const V *sl2 = sm + lB * a.LS;
 #pragma unroll
         for (int m = 0; m < P; m++) pts[m] = sl2[swz<LB>(tB + m * TPL)];
+        on_free(false);
+    } else if (!moved) {
+        on_free(false);
     }
 
     // ---- ring: every thread has consumed its loads (the exchanges above, or the
     //      barrier here); drop the ring lines this tile read from L2 without a
     //      write-back (discard.global.L2): the intermediate never reaches HBM
     if (LPL == 1 && a.ring == 1 && a.discard) {
-        __syncthreads();
+        sync();
         constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
         const int64_t io = b_io + int64_t(lA) * a.in_str[0] + ring_off;
         const E *in = reinterpret_cast<const E *>(a.in);
@@ -527,8 +551,8 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         // (DistStep kind 3; the readers run after it): one fence per CTA, after
         // the barrier -- the fence is cumulative over the CTA's stores that the
         // barrier ordered before it (per-thread fences cost 8 % in the loopback)
-        __syncthreads();
-        if (threadIdx.x == 0) __threadfence_system();
+        sync();
+        if (tid == 0) __threadfence_system();
         return;
     }
     {
@@ -584,7 +608,7 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
         const int64_t nt = int64_t(blockIdx.x) + a.pf_dist;
         if (nt < a.ntiles) prefetch_tile<V, LR>(a, nt * a.W * LPL);
     }
-    const TileMap mp = tile_map<TPL>(a);
+    const TileMap mp = tile_map<TPL>(a, threadIdx.x);
     int64_t b_io, b_oo, b_te;
     line_offsets(a, line0, b_io, b_oo, b_te);  // the tile's first line; line l adds l * str[0]
     int64_t io = b_io + int64_t(LPL * mp.lA) * a.in_str[0];
@@ -610,7 +634,218 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
             if constexpr (LPL == 2) pts[m].w = -pts[m].w;
         }
     }
-    tile_compute<V, LR>(a, line0, sm, ring_off, pts, b_io, b_oo, b_te);
+    tile_compute<V, LR>(a, line0, sm, ring_off, pts, b_io, b_oo, b_te, threadIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// Radix-32 steps on thread PAIRS with a warp-shuffle exchange (MOA_FFT_PAIR,
+// complex128 512- and 1024-point lines): each thread holds 16 points instead
+// of 32, so a CTA carries twice the warps at the same tile (the radix-32
+// in-thread kernels run 8 warps per SM at ~190 registers and are bound by
+// latency, profiles/r2b_cfg5_pass_ncu_full.txt).  A 32-point group j is split
+// by the parity h of its input index: thread h holds x_{2m+h} (m < 16),
+//   X[k' + 16 q] = E_0[k'] + (-1)^q w_32^{k'} E_1[k'],  E_h = DFT_16(x_{2m+h}),
+// (decimation in time; cf. the radix-2 stage B_L of Fig. vanloan_fft
+// P:1863-1873).  Thread 1 negates its odd inputs, so its DFT_16 comes out
+// rotated by 8; both threads then keep registers 0..7 and swap 8..15 with the
+// partner lane (8 complex values = 32 SHFL), and thread h finishes
+// X[8h + i] and X[16 + 8h + i] for i < 8.
+template <typename V> __device__ __forceinline__ V shfl_x(V v, int mask) {
+    V r;
+    r.x = __shfl_xor_sync(0xffffffffu, v.x, mask);
+    r.y = __shfl_xor_sync(0xffffffffu, v.y, mask);
+    return r;
+}
+template <int I, typename V> __device__ __forceinline__ void pair_tw(V (&v)[16]) {
+    if constexpr (I < 8) {
+        v[I] = rot32<8 + I>(v[I]);                  // E_1[8 + I] w_32^{8 + I}
+        if constexpr (I > 0) v[8 + I] = rot32<I>(v[8 + I]);  // E_1[I] w_32^I
+        pair_tw<I + 1>(v);
+    }
+}
+template <typename V> __device__ __forceinline__ void dft32_pair(V (&v)[16], int h, int xmask) {
+    if (h) {
+#pragma unroll
+        for (int m = 1; m < 16; m += 2) v[m] = mk<V>(-v[m].x, -v[m].y);
+    }
+    dft_reg<4>(v);
+    if (h) pair_tw<0>(v);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const V r = shfl_x(v[8 + i], xmask);
+        const V s = cadd(v[i], r);
+        V d = csub(v[i], r);
+        if (h) d = mk<V>(-d.x, -d.y);
+        v[i] = s;
+        v[8 + i] = d;
+    }
+}
+
+// The paired line DFT of R = 2^LR (9 or 10) points: step 0 (radix 32 on pairs)
+// in the load mapping, the exchange through shared memory (pad one per 32),
+// step 1 (R = 1024: radix 32 on pairs; R = 512: radix 16 in-thread, one group
+// per thread) in the store mapping with the step twiddles w_{32 Q}^{j r}.
+// Returns pts[m] = X[kb + s1 (m mod M1) + s2 (m / M1)] via kb / M1 / s1 / s2.
+template <int LR, typename V, typename Sync, typename OnFree>
+__device__ __forceinline__ void line_fft_pair(V (&pts)[16], V *sm, int LS, int lA, int pA, int xA, int lB, int pB,
+                                              int xB, const V *__restrict__ twR, const Sync &sync,
+                                              const OnFree &on_free) {
+    constexpr int R = 1 << LR;
+    {  // step 0: group j = pA / 2, inputs r = 2m + h (NS = 1): outputs at j 32 + r'
+        const int j = pA >> 1, h = pA & 1;
+        dft32_pair(pts, h, xA);
+        V *sl = sm + lA * LS;
+        const int base = j * 32 + 8 * h;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            sl[swz<5>(base + i)] = pts[i];
+            sl[swz<5>(base + 16 + i)] = pts[8 + i];
+        }
+    }
+    sync();
+    const V *sl = sm + lB * LS;
+    if constexpr (R == 1024) {
+        const int j = pB >> 1, h = pB & 1;
+#pragma unroll
+        for (int m = 0; m < 16; m++) pts[m] = sl[swz<5>(j + (2 * m + h) * 32)];
+        sync();
+        on_free(true);
+        // step twiddles w_1024^{j r}, r = 2m + h: w = w_1024^j (table entry NS + j - 1),
+        // v[m] *= w^h (w^2)^m as products A[a] B'[b], m = 4a + b, B'[b] = w^h (w^2)^b
+        if (j > 0) {
+            const V w1 = __ldg(twR + (32 + j - 1));
+            const V w2 = cmul(w1, w1);
+            const V base = h ? w1 : mk<V>(1.0, 0.0);
+            V B[4];
+            B[0] = base;
+            B[1] = cmul(base, w2);
+            const V w4 = cmul(w2, w2);
+            B[2] = cmul(base, w4);
+            B[3] = cmul(B[2], w2);
+            const V w8 = cmul(w4, w4);
+            V A = w8;
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+#pragma unroll
+                for (int b = 0; b < 4; b++) pts[4 * a + b] = cmul(pts[4 * a + b], a == 0 ? B[b] : cmul(A, B[b]));
+                if (a > 0 && a < 3) A = cmul(A, w8);
+            }
+        }
+        dft32_pair(pts, h, xB);
+    } else {  // R = 512: step 1 radix 16 in-thread, group j = pB (< 32), inputs j + 32 r
+        const int j = pB;
+#pragma unroll
+        for (int m = 0; m < 16; m++) pts[m] = sl[swz<5>(j + m * 32)];
+        sync();
+        on_free(true);
+        if (j > 0) {
+            const V w1 = __ldg(twR + (32 + j - 1));
+            const V w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
+            const V B[4] = {w1, w1, w2, w3};
+            V A = w4;
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int r = 4 * a + b;
+                    if (r == 0) continue;
+                    pts[r] = cmul(pts[r], a == 0 ? B[b] : (b == 0 ? A : cmul(A, B[b])));
+                }
+                if (a > 0 && a + 1 < 4) A = cmul(A, w4);
+            }
+        }
+        dft_reg<4>(pts);
+    }
+}
+
+// A tile of the paired variant: load (16 points per thread), line DFT, lifted
+// weights, store -- the plain kernel's tile with the paired mappings.
+template <int LR, typename Sync = CtaSync, typename OnFree = NoFree>
+__device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2 *sm, int tid, const Sync &sync = Sync(),
+                                          const OnFree &on_free = OnFree()) {
+    using V = double2;
+    constexpr int R = 1 << LR, P = 16, TPL = R / P;
+    // mappings: line-fast (lanes over the W lines; partner lane ^ W) or
+    // point-fast (lanes over the points; partner lane ^ 1)
+    const int lA = a.lf_load ? tid & (a.W - 1) : tid / TPL, pA = a.lf_load ? tid >> a.lW : tid % TPL;
+    const int lB = a.lf_store ? tid & (a.W - 1) : tid / TPL, pB = a.lf_store ? tid >> a.lW : tid % TPL;
+    const int xA = a.lf_load ? a.W : 1, xB = a.lf_store ? a.W : 1;
+    int64_t b_io, b_oo, b_te;
+    line_offsets(a, line0, b_io, b_oo, b_te);
+    // point index of register m in the load mapping: j + h R/32 + m R/16
+    const int tA = (pA >> 1) + (pA & 1) * (R / 32);
+    V pts[P];
+    {
+        const uint64_t pol = l2_policy(false);
+        const int64_t io = b_io + int64_t(lA) * a.in_str[0];
+        const char *ptr = reinterpret_cast<const char *>(reinterpret_cast<const V *>(a.in) + io + int64_t(tA) * a.in_kstr);
+        const int64_t stepb = int64_t(TPL) * a.in_kstr * int64_t(sizeof(V));
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+            pts[m] = ld_pol(reinterpret_cast<const V *>(ptr), pol);
+            ptr += stepb;
+        }
+    }
+    if (a.conj_in) {
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m].y = -pts[m].y;
+    }
+    const V *twR = reinterpret_cast<const V *>(a.twR);
+    line_fft_pair<LR>(pts, sm, a.LS, lA, pA, xA, lB, pB, xB, twR, sync, on_free);
+    // output index of register m: kb + S1 (m mod M1) + S2 (m / M1)
+    constexpr int S1 = 32, M1 = R == 1024 ? 8 : 16, S2 = 512;
+    const int kb = R == 1024 ? (pB >> 1) + 256 * (pB & 1) : pB;
+    // ---- lifted weights w_N^{(e k) mod N}: w_N^{e kb} (w_N^{e S1})^i (w_N^{e S2})^{m / M1}
+    int64_t oo = b_oo + int64_t(lB) * a.out_str[0];
+    if (a.twmask) {
+        const double2 *__restrict__ hi = reinterpret_cast<const double2 *>(a.tw_hi);
+        const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
+        const int64_t lmask = (int64_t(1) << a.twh) - 1;
+        const int64_t e0 = b_te + int64_t(lB) * a.tw_str[0] + a.tw_off;
+        auto tw = [&](int64_t e) {
+            e &= a.twmask;
+            return cmul(__ldg(hi + (e >> a.twh)), __ldg(lo + (e & lmask)));
+        };
+        const V w = tw(e0 * kb), s1 = tw(e0 * S1);
+        V start[P / M1];
+        start[0] = w;
+        if constexpr (P / M1 > 1) start[1] = cmul(w, tw(e0 * S2));
+        const V s2 = cmul(s1, s1), s3 = cmul(s2, s1), s4 = cmul(s2, s2);
+        const V B[4] = {mk<V>(1.0, 0.0), s1, s2, s3};
+#pragma unroll
+        for (int hlf = 0; hlf < P / M1; hlf++) {
+            V A = start[hlf];
+#pragma unroll
+            for (int ai = 0; ai < M1 / 4; ai++) {
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int m = hlf * M1 + ai * 4 + b;
+                    pts[m] = cmul(pts[m], b ? cmul(A, B[b]) : A);
+                }
+                if (ai + 1 < M1 / 4) A = cmul(A, s4);
+            }
+        }
+    }
+    if (a.conj_out || a.scale != 1.0) {
+        const double sr = a.scale, si = a.conj_out ? -a.scale : a.scale;
+#pragma unroll
+        for (int m = 0; m < P; m++) pts[m] = mk<V>(pts[m].x * sr, pts[m].y * si);
+    }
+    // ---- store
+    const uint64_t pol = l2_policy(false);
+    V *out = reinterpret_cast<V *>(a.out);
+#pragma unroll
+    for (int m = 0; m < P; m++) {
+        const int k = kb + S1 * (m % M1) + S2 * (m / M1);
+        const int64_t off = a.ksplit >= LR ? int64_t(k) * a.out_kstr : kaddr(a, k);
+        st_pol(out + oo + off, pts[m], pol);
+    }
+}
+
+template <int LR>
+__global__ void __launch_bounds__(256, 2) pass_kernel_pair(const KArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    tile_pair<LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<double2 *>(smem_raw), threadIdx.x);
 }
 
 template <typename V, int LR>
@@ -619,6 +854,243 @@ template <typename V, int LR>
 __global__ void __launch_bounds__(lp_of<V, LR>() == 5 ? 256 : 512) pass_kernel(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
+}
+
+// ---------------------------------------------------------------------------
+// Asynchronously fed pass kernel (MOA_FFT_WS): the loads of a tile are taken
+// off the compute warps' critical path.  One persistent CTA per SM with a ring
+// of S shared-memory stages, each fed by TMA -- a tensor-map box of W
+// adjacent lines x 256 points per copy for a line-fast (strided) side
+// (cp.async.bulk.tensor), one bulk copy per line for contiguous lines
+// (cp.async.bulk) -- completing on the stage's mbarrier.  Two consumer warp
+// groups take the stages' tiles alternately (tile sequence k = g, g + 2, ...):
+// read the landed tile in the load mapping, run the block butterflies /
+// lifted weights exactly as the plain kernel (tile_compute, with a named
+// barrier over the group), reusing the stage as the exchange buffer, and store
+// with 128-bit register stores.  The moment a group has read its stage for the
+// last time it refills it with tile k + S (one elected thread issues the
+// copies; no producer warp, so the kernel keeps the plain kernel's register
+// budget).  Tiles come in order from an atomic counter (reset before every
+// launch; fetched while the current tile computes), so the CTAs stay on
+// neighbouring tiles and the DRAM access order matches the plain kernel's.
+// The paper's prefetch argument: with the next tiles already in
+// flight, "pre-fetching becomes a deterministic cost" off the critical path.
+constexpr int kWsStagesMax = 4;
+constexpr int kWsGroupMax = 128;  // threads per consumer group
+// (the lifted-weight table entries are fetched after the butterflies: holding
+// them across the DFT costs registers the stage pipeline already hides)
+constexpr bool kWsEarlyTw = false;
+struct alignas(64) WsArgs {
+    CUtensorMap tmap;  // line-fast loads: dims (2 W-lines reals, points, line digits 1..)
+    KArgs a;
+    int64_t ntiles;
+    unsigned long long *ctr;  // tile counter (null: static round-robin)
+    int32_t stages, stage_elems, mode;  // mode 0: tensor-map boxes; 1: one bulk copy per line
+    int32_t nbox, box_pts, tmap_rank;
+    int32_t ext0;                        // extent of line digit 0 (tensor dims)
+    uint32_t stage_bytes;                // bytes landed per tile
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// (a watchdog turns a broken pipeline into a launch error instead of a hang)
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(b, parity)) {
+        if (++spins == (1u << 24)) {
+            printf("moa ws watchdog: block %d thread %d barrier %p parity %u\n", blockIdx.x, threadIdx.x, (void *)b,
+                   parity);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_tensor_g2s(void *dst, const void *tmap, int rank, const int32_t (&c)[5], uint64_t *bar) {
+    const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+    const uint64_t t = reinterpret_cast<uint64_t>(tmap);
+    switch (rank) {
+        case 2:
+            asm volatile("cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(d),
+                         "l"(t), "r"(c[0]), "r"(c[1]), "r"(b)
+                         : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d),
+                         "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
+                         : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.tensor.4d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(d),
+                         "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b)
+                         : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.tensor.5d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d),
+                         "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+                         : "memory");
+            break;
+    }
+}
+
+// Tile index of the CTA's k-th tile: the counter (dynamic, in order) or static
+// round-robin.
+__device__ __forceinline__ int64_t ws_next_tile(const WsArgs &w, int64_t k) {
+    if (w.ctr) return int64_t(atomicAdd(w.ctr, 1ull));
+    return int64_t(blockIdx.x) + k * gridDim.x;
+}
+
+// Fill stage s with tile `tile` (or the end marker -1): the tile's copies
+// complete on full[s] together with the arrival.
+// tile_of[0] = the tile (-1: end), tile_of[1] = its sequence number k: a
+// consumer checks k after the barrier, since a stage's consecutive rounds
+// alternate between the two groups and a phase parity alone could alias a
+// round two phases back.
+template <typename V, int LR>
+__device__ __forceinline__ void ws_fill(const WsArgs &w, V *stage, uint64_t *full, int64_t *tile_of, int64_t tile,
+                                        int64_t k) {
+    using E = typename ElemOf<V>::type;
+    constexpr int R = 1 << LR;
+    const KArgs &a = w.a;
+    reinterpret_cast<volatile int64_t *>(tile_of)[1] = k;
+    if (tile >= w.ntiles) {
+        reinterpret_cast<volatile int64_t *>(tile_of)[0] = -1;
+        mbar_arrive(full);
+        return;
+    }
+    reinterpret_cast<volatile int64_t *>(tile_of)[0] = tile;
+    mbar_arrive_tx(full, w.stage_bytes);
+    const int64_t line0 = tile * a.W;
+    if (w.mode == 0) {
+        // coordinates: (2 digit0 reals, point, digit 1, ...)
+        int32_t c[5] = {0, 0, 0, 0, 0};
+        int64_t rest = line0;
+        c[0] = int32_t(2 * (rest % w.ext0));
+        rest /= w.ext0;
+        for (int i = 1; i < a.ndig && i + 1 < 5; i++) {
+            c[i + 1] = int32_t(rest & ((int64_t(1) << a.lext[i]) - 1));
+            rest >>= a.lext[i];
+        }
+        for (int b = 0; b < w.nbox; b++) {
+            c[1] = b * w.box_pts;
+            tma_tensor_g2s(stage + size_t(b) * w.box_pts * a.W, &w.tmap, w.tmap_rank, c, full);
+        }
+    } else {
+        int64_t io, oo, te;
+        line_offsets(a, line0, io, oo, te);
+        const E *in = reinterpret_cast<const E *>(a.in) + io;
+        for (int l = 0; l < a.W; l++)
+            tma_bulk_g2s(stage + size_t(l) * a.LS, in + int64_t(l) * a.in_str[0], uint32_t(R * sizeof(E)), full);
+    }
+}
+
+// A consumer group's hand-back of its stage: every thread has read it for the
+// last time; the generic-proxy accesses are ordered before the async-proxy
+// (TMA) writes of the refill, which one elected thread then issues.
+template <typename V, int LR>
+struct WsRefill {
+    const WsArgs *w;
+    V *stage;
+    uint64_t *full;
+    int64_t *tile_of;
+    int64_t next;  // the tile for this stage's next round (valid on gtid 0)
+    int64_t knext;  // its sequence number
+    GroupSync sync;
+    int gtid;
+    __device__ __forceinline__ void operator()(bool) const {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sync();
+        if (gtid == 0) ws_fill<V, LR>(*w, stage, full, tile_of, next, knext);
+    }
+};
+
+template <typename V, int LR>
+__global__ void __launch_bounds__(2 * kWsGroupMax, 1) ws_pass_kernel(const __grid_constant__ WsArgs w) {
+    constexpr int LP = lp_of<V, LR>();
+    constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
+    const KArgs &a = w.a;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
+    int64_t *tile_of = reinterpret_cast<int64_t *>(full + kWsStagesMax);  // [stage][tile, k]
+    V *stage0 = reinterpret_cast<V *>(smem_raw + 128);
+    const int S = w.stages;
+    const int nthr = a.W * TPL;  // threads per consumer group
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) mbar_init(full + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < S; s++)
+            ws_fill<V, LR>(w, stage0 + size_t(s) * w.stage_elems, full + s, tile_of + 2 * s, ws_next_tile(w, s), s);
+    // ---- consumer group g takes the tiles k = g, g + 2, ...
+    const int g = threadIdx.x >= nthr;
+    const int gtid = threadIdx.x - g * nthr;
+    const GroupSync gsync{1 + g, nthr};
+    const TileMap mp = tile_map<TPL>(a, gtid);
+    for (int64_t k = g;; k += 2) {
+        const int s = int(k % S);
+        V *sm = stage0 + size_t(s) * w.stage_elems;
+        volatile int64_t *tag = tile_of + 2 * s;
+        do {
+            mbar_wait(full + s, uint32_t(k / S) & 1);
+        } while (tag[1] != k);
+        const int64_t tile = tag[0];
+        gsync();  // every thread has read the tag before the stage can be refilled
+        if (tile < 0) {  // pass the end marker on to the stage's next round, then stop
+            if (gtid == 0) ws_fill<V, LR>(w, sm, full + s, tile_of + 2 * s, w.ntiles, k + S);
+            break;
+        }
+        // this stage's next tile: fetched now, used at the refill (its latency
+        // hides behind this tile's butterflies)
+        const int64_t next = gtid == 0 ? ws_next_tile(w, k + S) : 0;
+        const int64_t line0 = tile * a.W;
+        int64_t b_io, b_oo, b_te;
+        line_offsets(a, line0, b_io, b_oo, b_te);
+        // the landed tile, in the load mapping: point tA + m TPL of line lA
+        V pts[P];
+        if (w.mode == 0) {
+            const V *src = sm + mp.tA * a.W + mp.lA;
+#pragma unroll
+            for (int m = 0; m < P; m++) pts[m] = src[m * TPL * a.W];
+        } else {
+            const V *src = sm + mp.lA * a.LS + mp.tA;
+#pragma unroll
+            for (int m = 0; m < P; m++) pts[m] = src[m * TPL];
+        }
+        if (a.conj_in) {
+#pragma unroll
+            for (int m = 0; m < P; m++) pts[m].y = -pts[m].y;
+        }
+        gsync();  // every dense read done before the exchange reuses the stage
+        tile_compute<V, LR, GroupSync, WsRefill<V, LR>, kWsEarlyTw>(
+            a, line0, sm, 0, pts, b_io, b_oo, b_te, gtid, gsync,
+            WsRefill<V, LR>{&w, sm, full + s, tile_of + 2 * s, next, k + S, gsync, gtid});
+    }
 }
 
 // A fused pass pair: pass A writes its output to an L2-resident ring of
@@ -916,15 +1388,134 @@ void set_prefetch(KArgs &a, const void *fn, int threads, int smem, int64_t tiles
     a.ntiles = tiles;
 }
 
+// ---- warp-specialised launch (MOA_FFT_WS != 0): eligible passes only, else
+// cudaErrorNotSupported and the plain kernel runs
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return EncodeTiledFn(nullptr);
+        }
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+int ws_mode() {  // MOA_FFT_WS: 0 off, 1 on (eligible passes)
+    const char *e = std::getenv("MOA_FFT_WS");
+    return e ? std::atoi(e) : 0;
+}
+
+template <typename V, int... Ls> constexpr auto make_ws_table(std::integer_sequence<int, Ls...>) {
+    return std::array<void (*)(const WsArgs), sizeof...(Ls)>{&ws_pass_kernel<V, Ls>...};
+}
+const std::array<void (*)(const WsArgs), 13> kWs128 = make_ws_table<double2>(std::make_integer_sequence<int, 13>{});
+const std::array<void (*)(const WsArgs), 13> kWs64 = make_ws_table<float2>(std::make_integer_sequence<int, 13>{});
+
+template <typename V>
+cudaError_t launch_ws(const std::array<void (*)(const WsArgs), 13> &tab, const moa_pass_desc_t &d, const KArgs &a,
+                      int64_t tiles, const DevTables &tb, cudaStream_t stream, const PassMods &mods) {
+    using E = typename ElemOf<V>::type;
+    const int esize = int(sizeof(E));
+    const int LP = psi_log_p(d.logR, sizeof(E) == 16 ? MOA_C128 : MOA_C64);
+    const int64_t R = int64_t(1) << d.logR, TPL = R >> LP;
+    const int64_t nthr = int64_t(d.W) * TPL;
+    if (d.ring || mods.npeers || d.kind > 1 || nthr > kWsGroupMax || nthr % 32 || d.ndig < 1) return cudaErrorNotSupported;
+    if (!std::is_same<V, double2>::value && !std::is_same<V, float2>::value) return cudaErrorNotSupported;
+    // short lines: a tile is many small copies (measured: 4-point lines, 128
+    // 64-byte copies per tile, 7x slower than the plain kernel)
+    if (d.logR < 8) return cudaErrorNotSupported;
+    // two consumer groups of >= 4 warps (one line per CTA of a 1024-point
+    // complex64 pass would leave 2 warps per SM: measured 4x slower)
+    if (nthr < 128) return cudaErrorNotSupported;
+    WsArgs w{};
+    w.a = a;
+    w.a.pf_dist = 0;
+    w.ntiles = tiles;
+    w.ctr = tb.ctr;
+    int mode;
+    if (d.lf_load && d.in_str[0] == 1 && d.ndig <= 4 && (int64_t(d.W) * esize) % 16 == 0) mode = 0;
+    else if (!d.lf_load && d.in_kstr == 1 && (int64_t(a.LS) * esize) % 16 == 0 && (R * esize) % 16 == 0) mode = 1;
+    else return cudaErrorNotSupported;
+    w.mode = mode;
+    w.stage_elems = int32_t(int64_t(d.W) * a.LS);
+    w.stage_bytes = uint32_t(int64_t(d.W) * R * esize);
+    // stages: as many as fit next to the 128-byte barrier block (<= 4)
+    int dev = 0, smem_max = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t stage_b = int64_t(w.stage_elems) * esize;
+    int S = int((smem_max - 128) / stage_b);
+    if (const char *se = std::getenv("MOA_FFT_WS_STAGES")) S = std::min(S, std::atoi(se));
+    if (S > kWsStagesMax) S = kWsStagesMax;
+    if (S < 2) return cudaErrorNotSupported;
+    w.stages = S;
+    if (mode == 0) {
+        EncodeTiledFn enc = encode_tiled();
+        if (!enc) return cudaErrorNotSupported;
+        cuuint64_t dims[5], strides[4];
+        cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+        int rank = 0;
+        dims[rank] = cuuint64_t(2 * d.ext[0]);
+        box[rank++] = cuuint32_t(2 * d.W);
+        const int64_t bp = R < 256 ? R : 256;
+        dims[rank] = cuuint64_t(R);
+        strides[rank - 1] = cuuint64_t(d.in_kstr * esize);
+        box[rank++] = cuuint32_t(bp);
+        for (int i = 1; i < d.ndig; i++) {
+            dims[rank] = cuuint64_t(d.ext[i]);
+            strides[rank - 1] = cuuint64_t(d.in_str[i] * esize);
+            box[rank++] = 1;
+        }
+        for (int i = 0; i < rank - 1; i++)
+            if (strides[i] % 16 || strides[i] >= (cuuint64_t(1) << 40)) return cudaErrorNotSupported;
+        CUresult r = enc(&w.tmap, esize == 16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         cuuint32_t(rank), const_cast<void *>(a.in), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
+        w.tmap_rank = rank;
+        w.nbox = int32_t(R / bp);
+        w.box_pts = int32_t(bp);
+        w.ext0 = int32_t(d.ext[0]);
+    }
+    auto fn = tab[d.logR];
+    const int smem = int(128 + S * stage_b);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (w.ctr) {
+        e = cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t grid = tiles < sms ? tiles : sms;
+    fn<<<dim3(unsigned(grid)), dim3(unsigned(2 * nthr)), size_t(smem), stream>>>(w);
+    return cudaGetLastError();
+}
+
 template <typename V>
 cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d, const void *in, void *out,
                      const DevTables &tb, cudaStream_t stream, const PassMods &mods) {
     int64_t nlines = 0;
     KArgs a = fill_args(d, in, out, tb, &nlines, mods, int(sizeof(typename ElemOf<V>::type)));
     const int64_t tiles = nlines / d.W;
-    // MOA_FFT_PF = f: prefetch the tile f * (resident CTAs) ahead into L2 (0: off)
-    double pf = 0.0;
-    if (const char *pe = std::getenv("MOA_FFT_PF")) pf = std::atof(pe);
+    // MOA_FFT_PF = f: prefetch the tile f * (resident CTAs) ahead into L2 (0: off),
+    // for contiguous-line (point-fast) loads -- a few large bulk prefetches per
+    // tile.  Line-fast loads would need one 128-byte prefetch per point, which
+    // measured slower (cfg3 4.95 -> 5.8 ms, cfg4 12.0 -> 13.4 ms,
+    // profiles/r2b_ab_pf.jsonl); MOA_FFT_PF_LF = f enables them (ablation).
+    // Default: 0.5 for contiguous lines of >= 512 points (measured: cfg5 passes
+    // 6.35 -> 6.22 ms, cfg3's 1024-point last pass 1.71 -> 1.57 ms; cfg2's
+    // 256-point rows 0.311 -> 0.315 ms, so not there -- profiles/r2c_ab_cfg5.jsonl,
+    // r2b_ab_pf.jsonl).
+    double pf = (!d.lf_load && d.logR >= 9) ? 0.5 : 0.0;
+    if (const char *pe = std::getenv(d.lf_load ? "MOA_FFT_PF_LF" : "MOA_FFT_PF")) pf = std::atof(pe);
     // complex64 passes of >= 2^10-point lines coalesced along the lines on both
     // sides (digit 0 unit stride in and out, even tile width): two adjacent
     // lines per lane -- half the threads and memory instructions per tile
@@ -980,6 +1571,26 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             f<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads / 2)), size_t(d.smem_bytes), stream>>>(b);
             return cudaGetLastError();
         }
+    }
+    // MOA_FFT_PAIR=1: complex128 512- / 1024-point lines on thread pairs
+    // (radix 32 with a warp-shuffle exchange, twice the threads per tile)
+    if constexpr (std::is_same<V, double2>::value) {
+        const char *pe = std::getenv("MOA_FFT_PAIR");
+        if (pe && pe[0] == '1' && (d.logR == 9 || d.logR == 10) && d.kind == 0 && !d.ring && !mods.npeers &&
+            2 * d.threads <= 256) {
+            auto fn = d.logR == 9 ? &pass_kernel_pair<9> : &pass_kernel_pair<10>;
+            if (d.smem_bytes > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
+                if (e != cudaSuccess) return e;
+            }
+            fn<<<dim3(unsigned(tiles)), dim3(unsigned(2 * d.threads)), size_t(d.smem_bytes), stream>>>(a);
+            return cudaGetLastError();
+        }
+    }
+    if (ws_mode() && d.W >= 1) {
+        cudaError_t e = std::is_same<V, double2>::value ? launch_ws<V>(kWs128, d, a, tiles, tb, stream, mods)
+                                                        : launch_ws<V>(kWs64, d, a, tiles, tb, stream, mods);
+        if (e != cudaErrorNotSupported) return e;
     }
     KFn<V> fn = tab[d.logR];
     if (d.smem_bytes > 48 * 1024) {

@@ -50,6 +50,7 @@ struct DevTables {
     const void *twR = nullptr;   // this pass's in-line Stockham step twiddles (step-major, R - 1 entries)
     const void *tw_hi = nullptr; // w_N^{eh 2^h}
     const void *tw_lo = nullptr; // w_N^{el}
+    unsigned long long *ctr = nullptr;  // this pass's tile counter (warp-specialised kernel), or null
 };
 // Device state of the L2 ring of a fused pass pair (owned by the plan).
 struct RingState {

@@ -11,6 +11,7 @@ JSON line per (case, variant, round): total ms per exec (CUDA events over
 import argparse
 import json
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -18,6 +19,7 @@ import torch  # noqa: E402
 
 import paper_0803_2386_b200 as m  # noqa: E402
 
+LAST_CLK = {}
 CASES = {
     "cfg2": dict(n=1 << 16, batch=1024, dtype="c128"),
     "cfg3": dict(n=1 << 28, batch=1, dtype="c128"),
@@ -42,6 +44,48 @@ def parse_case(s):
     return c
 
 
+class Nvml:
+    """SM clock / power samples during a timed region (median)."""
+
+    def __init__(self):
+        import threading
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(0)
+            self.ok = True
+        except Exception:
+            pass
+        self.threading = threading
+
+    def __enter__(self):
+        self.clk, self.pw, self.stop = [], [], self.threading.Event()
+        if self.ok:
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        self.clk.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                        self.pw.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                    except Exception:
+                        pass
+                    self.stop.wait(0.002)
+            self.t = self.threading.Thread(target=loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.clk:
+            return {}
+        c, p = sorted(self.clk), sorted(self.pw)
+        return {"sm_mhz": c[len(c) // 2], "power_w": round(p[len(p) // 2], 1), "samples": len(c)}
+
+
 def run(case, reps):
     if "shape" in case:
         plan = m.FFTPlan.plan_3d(*case["shape"], dtype=case["dtype"])
@@ -55,11 +99,14 @@ def run(case, reps):
     torch.cuda.synchronize()
     m.moa_fft_prof_begin(plan.h, reps)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        plan.exec(x, y)
-    e1.record()
-    torch.cuda.synchronize()
+    with Nvml() as nv:
+        e0.record()
+        for _ in range(reps):
+            plan.exec(x, y)
+        e1.record()
+        torch.cuda.synchronize()
+    global LAST_CLK
+    LAST_CLK = nv.summary()
     per, nex = m.moa_fft_prof_end(plan.h)
     desc = [(1 << d["logR"], d["W"], d["threads"]) for d in plan.describe()]
     plan.close()
@@ -84,12 +131,12 @@ def main():
                 name, _, envs = v.partition(":")
                 os.environ.clear()
                 os.environ.update(base_env)
-                for kv in filter(None, envs.split(",")):
+                for kv in filter(None, re.split(r",(?=[A-Z_0-9]+=)", envs)):
                     k, _, val = kv.partition("=")
                     os.environ[k] = val
                 try:
                     ms, per, desc = run(case, a.reps)
-                    print(json.dumps({"case": cs, "variant": name, "env": envs, "round": rnd, "ms": round(ms, 4),
+                    print(json.dumps({"case": cs, "variant": name, "env": envs, "round": rnd, "ms": round(ms, 4), "clk": LAST_CLK,
                                       "per_launch_ms": per, "passes": desc}), flush=True)
                 except Exception as ex:  # keep sweeping
                     print(json.dumps({"case": cs, "variant": name, "env": envs, "round": rnd, "error": str(ex)}),
