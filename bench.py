@@ -296,6 +296,14 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
     barrier()
 
     launches = plan.launches
+    # the timed calls go straight to the C-ABI entry point (moa_fft_exec through
+    # ctypes, pointers and stream resolved once): for the latency-bound cfg1 the
+    # Python wrapper's argument checks would otherwise be part of every step
+    xp, yp, sh, ph = x.data_ptr(), y.data_ptr(), stream.cuda_stream, plan.h
+
+    def run_exec():
+        m.moa_fft_exec(ph, xp, yp, sh)
+
     m.moa_fft_prof_begin(plan.h, steps)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)] if small else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,14 +313,14 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
             for i in range(steps):
                 flush.fill_(i & 0xFF)                        # evict L2 between timed iterations
                 ev[2 * i].record(stream)
-                plan.exec(x, y, stream)
+                run_exec()
                 ev[2 * i + 1].record(stream)
             barrier()
             total_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(steps))
         else:
             start.record(stream)
             for _ in range(steps):
-                plan.exec(x, y, stream)
+                run_exec()
             end.record(stream)
             barrier()
             total_ms = start.elapsed_time(end)
@@ -439,7 +447,8 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
                 a1.synchronize()
                 ts.append(a0.elapsed_time(a1) * 1e3)
             return round(sorted(ts)[len(ts) // 2], 2)
-        plain_us = med(lambda: plan.exec(x, y, stream))
+        plain_us = med(run_exec)
+        wrapper_us = med(lambda: plan.exec(x, y, stream))
         try:
             g = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
@@ -453,7 +462,19 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
             graph_us = med(g.replay)
         except Exception as ex:  # pragma: no cover
             graph_us = f"capture failed: {ex}"
-        latency = {"plain_launch_us": plain_us, "cuda_graph_us": graph_us, "l2": "warm", "reps": 1000}
+        # and with L2 flushed before each call (the timed region's condition)
+        fl = []
+        for i in range(200):
+            flush.fill_(i & 0xFF)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            run_exec()
+            a1.record(stream)
+            a1.synchronize()
+            fl.append(a0.elapsed_time(a1) * 1e3)
+        latency = {"plain_launch_us": plain_us, "plain_launch_l2_flushed_us": round(sorted(fl)[len(fl) // 2], 2),
+                   "python_wrapper_us": wrapper_us, "cuda_graph_us": graph_us, "l2": "warm unless stated",
+                   "reps": 1000, "how": "CUDA events around one moa_fft_exec C-ABI call (ctypes), median"}
 
     err = None
     if ctx["cpu_leg"]:

@@ -1235,6 +1235,111 @@ __global__ void __launch_bounds__((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5)
 }
 
 // ---------------------------------------------------------------------------
+// Latency form of a one-pass plan with few lines (cfg1: one 2^10-point
+// transform).  One CTA per line, R/4 threads: radix-4 Stockham steps (the
+// self-sorting form of the radix-2 network, Fig. vanloan_fft, two
+// stages per step) ping-ponging between two shared-memory buffers, one barrier
+// per step; the table w_R^e (e < 3R/4) is computed in the prologue with
+// sincospi while the line's loads are in flight, so no dependent table load
+// waits on DRAM; the first step runs straight from the loaded registers and the
+// last one stores to global memory in natural order.
+template <typename V> __device__ __forceinline__ V tw_exact(int e, int R);
+template <> __device__ __forceinline__ double2 tw_exact<double2>(int e, int R) {
+    double s, c;
+    sincospi(2.0 * double(e) / double(R), &s, &c);
+    return make_double2(c, -s);
+}
+template <> __device__ __forceinline__ float2 tw_exact<float2>(int e, int R) {
+    // complex64: the angle in double, rounded once (~1 ulp of float)
+    double s, c;
+    sincospi(2.0 * double(e) / double(R), &s, &c);
+    return make_float2(float(c), float(-s));
+}
+__device__ __forceinline__ int spad(int i) { return i + (i >> 4); }  // one pad element per 16
+
+template <typename V, int LR>
+__global__ void __launch_bounds__((1 << LR) / 4) small_fft_kernel(const KArgs a) {
+    constexpr int R = 1 << LR, T = R / 4, NT4 = LR / 2;  // radix-4 steps; odd LR adds a radix-2 step
+    constexpr bool R2 = (LR & 1) != 0;
+    constexpr int TW = 3 * R / 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V *buf0 = reinterpret_cast<V *>(smem_raw);
+    V *buf1 = buf0 + spad(R);
+    V *tw = buf1 + spad(R);
+    using E = typename ElemOf<V>::type;
+    const int t = threadIdx.x;
+    int64_t io, oo, te;
+    line_offsets(a, int64_t(blockIdx.x), io, oo, te);
+    const E *in = reinterpret_cast<const E *>(a.in) + io;
+    V v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) v[q] = in[t + q * T];
+    for (int e = t; e < TW; e += T) tw[e] = tw_exact<V>(e, R);
+    if (a.conj_in) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q].y = -v[q].y;
+    }
+    __syncthreads();
+    V *src = buf0, *dst = buf1;
+    int NS = 1;
+#pragma unroll
+    for (int s = 0; s < NT4; s++) {
+        if (s > 0) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = src[spad(t + q * T)];
+            // twiddles w_{4 NS}^{k q} = w_R^{k q R / (4 NS)}
+            const int k = t & (NS - 1), st = R / (4 * NS);
+#pragma unroll
+            for (int q = 1; q < 4; q++) v[q] = cmul(v[q], tw[k * q * st]);
+        }
+        // radix-4 DFT (w_4 = -i)
+        const V a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
+        const V mb1 = mk<V>(b1.y, -b1.x);  // -i b1
+        V y[4] = {cadd(a0, b0), cadd(a1, mb1), csub(a0, b0), csub(a1, mb1)};
+        const int base = ((t / NS) * 4 * NS) + (t & (NS - 1));
+        const bool last = !R2 && s == NT4 - 1;
+        if (!last) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) dst[spad(base + r * NS)] = y[r];
+            __syncthreads();
+            V *x = src;
+            src = dst;
+            dst = x;
+            NS *= 4;
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; r++) v[r] = y[r];
+            NS *= 4;
+        }
+    }
+    int kb = t, ks = T;  // outputs: v[q] = X[kb + q ks]
+    if constexpr (R2) {  // final radix-2 step: NS = R/2, each thread two groups j = t, t + T
+        V w[4];
+#pragma unroll
+        for (int g = 0; g < 2; g++) {
+            const int j = t + g * T;
+            V x0 = src[spad(j)], x1 = src[spad(j + R / 2)];
+            x1 = cmul(x1, tw[j]);  // w_R^{j}
+            w[g] = cadd(x0, x1);
+            w[2 + g] = csub(x0, x1);
+        }
+        // X[j] = w[g], X[j + R/2] = w[2 + g]: q -> k = t + q T
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = w[q];
+    }
+    V *out = reinterpret_cast<V *>(a.out) + oo;
+    const bool mod = a.conj_out || a.scale != 1.0;
+    using Tr = typename RealOf<V>::type;
+    const Tr sr = Tr(a.scale), si = a.conj_out ? -Tr(a.scale) : Tr(a.scale);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        V r = v[q];
+        if (mod) r = mk<V>(r.x * sr, r.y * si);
+        out[kb + q * ks] = r;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // The unblocked control (MOA_FFT_UNBLOCKED): Van Loan's program as written,
 // Fig. vanloan_fft P:1845-1876 -- x <- P_n x, then for q = 1..t one global
 // radix-2 stage x_{L x r} <- B_L x_{L x r} (L = 2^q), each a full HBM round
@@ -1569,6 +1674,34 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             }
             if (pf > 0 && !d.ring) set_prefetch(b, reinterpret_cast<const void *>(f), d.threads / 2, d.smem_bytes, tiles, pf);
             f<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads / 2)), size_t(d.smem_bytes), stream>>>(b);
+            return cudaGetLastError();
+        }
+    }
+    // one-pass plans with few lines (latency, cfg1): the small-transform kernel
+    // (MOA_FFT_SMALL=0 disables it)
+    if (d.kind == 0 && !d.ring && !mods.npeers && d.twN <= 1 && d.logR >= 6 && d.logR <= 12 && !d.lf_load &&
+        !d.lf_store && d.in_kstr == 1 && d.out_kstr == 1 && d.out_ksplit >= d.logR && nlines <= 64) {
+        const char *se = std::getenv("MOA_FFT_SMALL");
+        if (!(se && se[0] == '0')) {
+            static const std::array<KFn<V>, 7> small = {&small_fft_kernel<V, 6>, &small_fft_kernel<V, 7>,
+                                                        &small_fft_kernel<V, 8>, &small_fft_kernel<V, 9>,
+                                                        &small_fft_kernel<V, 10>, &small_fft_kernel<V, 11>,
+                                                        &small_fft_kernel<V, 12>};
+            const int R = 1 << d.logR;
+            const size_t smem = (2 * size_t(R + (R >> 4)) + size_t(3 * R / 4)) * sizeof(V);
+            KFn<V> fn = small[d.logR - 6];
+            static std::mutex mu;
+            static std::map<const void *, size_t> attr;  // opt-in shared memory set once per kernel
+            if (smem > 48 * 1024) {
+                std::lock_guard<std::mutex> g(mu);
+                size_t &have = attr[reinterpret_cast<const void *>(fn)];
+                if (have < smem) {
+                    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                    if (e != cudaSuccess) return e;
+                    have = smem;
+                }
+            }
+            fn<<<dim3(unsigned(nlines)), dim3(unsigned(R / 4)), smem, stream>>>(a);
             return cudaGetLastError();
         }
     }

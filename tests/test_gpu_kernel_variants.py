@@ -107,3 +107,22 @@ def test_variant_cfg3_full(m, torch_cuda, monkeypatch, env):
     y = run(torch_cuda, m.FFTPlan(n, 1, "c128"), x)
     ref = oracle.fft_radix2(x)
     assert rel_l2(y, ref) <= 1e-11
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("t,batch", [(6, 1), (7, 3), (8, 1), (9, 64), (10, 1), (10, 7), (11, 2), (12, 5)])
+def test_small_kernel_vs_oracle_and_plain(m, torch_cuda, monkeypatch, dtype, t, batch):
+    # the latency form of one-pass plans with few lines (cfg1's 2^10), forward
+    # and inverse-normalised, against the oracle and the throughput kernel
+    n = 1 << t
+    x = synth.fill(n * batch, 35, synth.UNIFORM, dtype)
+    ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+    monkeypatch.setenv("MOA_FFT_SMALL", "1")
+    y = run(torch_cuda, m.FFTPlan(n, batch, dtype), x)
+    assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype]
+    yi = run(torch_cuda, m.FFTPlan(n, batch, dtype, inverse=True, normalize=True), x)
+    refi = oracle.fft_radix2_rows_sign(x.astype(np.complex128), n, +1) / n
+    assert rel_l2(yi.astype(np.complex128), refi) <= TOL[dtype]
+    monkeypatch.setenv("MOA_FFT_SMALL", "0")
+    y0 = run(torch_cuda, m.FFTPlan(n, batch, dtype), x)
+    assert rel_l2(y.astype(np.complex128), y0.astype(np.complex128)) <= TOL[dtype]

@@ -17,6 +17,7 @@ from tools.ab_env import Nvml, parse_case  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("case")
 ap.add_argument("--reps", type=int, default=30)
+ap.add_argument("--seconds", type=float, default=3.0, help="run each leg this long; NVML samples its second half")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 case = parse_case(a.case)
@@ -30,17 +31,28 @@ desc = plan.describe()
 
 
 def timed(fn, label):
+    import time
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    one = max(time.time() - t0, 1e-4)
+    reps = max(a.reps, int(a.seconds / 2 / one))
+    for _ in range(reps):                      # first half: reach the power / thermal steady state
+        fn()
+    torch.cuda.synchronize()
     with Nvml() as nv:
         e0.record()
-        for _ in range(a.reps):
+        for _ in range(reps):
             fn()
         e1.record()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.reps
+    ms = e0.elapsed_time(e1) / reps
     c = nv.summary()
     print(json.dumps({"case": a.case, "what": label, "ms": round(ms, 4), **c,
                       "mJ": round(ms * c.get("power_w", 0), 1)}), flush=True)
