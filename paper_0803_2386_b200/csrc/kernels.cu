@@ -50,24 +50,58 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cmul(double2 a, double2 w) {
     return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
 }
+// complex64 arithmetic on the packed FP32x2 pipe (sm_100: FADD2 / FMUL2 /
+// FFMA2 -- one instruction per complex add, two per complex multiply; ptxas
+// folds the operand swap and the broadcast of w.x / w.y into the instruction's
+// operand modifiers, so no register moves).  The complex64 passes are
+// instruction-issue bound, and this halves their FP32 count.
+// MOA_FFT_NO_F32X2 (compile-time) restores the scalar forms for ablation.
+#ifndef MOA_FFT_NO_F32X2
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {  // (a.x w.x - a.y w.y, a.y w.x + a.x w.y)
+    unsigned long long t, d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2(a.x, a.y)), "l"(pk2(w.x, w.x)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a.y, a.x)), "l"(pk2(-w.y, w.y)), "l"(t));
+    return upk2(d);
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 w) {
     return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
 }
+#endif
 // Paired complex64 lines: two ADJACENT lines of a line-coalesced complex64
 // pass in one 16-byte quad (re0, im0, re1, im1) -- one 128-bit load / store /
 // exchange per two points and one set of step twiddles and address
 // arithmetic for both lines (the complex64 passes are issue-bound).
-__device__ __forceinline__ float4 cadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-__device__ __forceinline__ float4 csub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
-__device__ __forceinline__ float4 cmul(float4 a, float2 w) {
-    return make_float4(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x), fmaf(a.z, w.x, -a.w * w.y),
-                       fmaf(a.z, w.y, a.w * w.x));
-}
+__device__ __forceinline__ float4 f4(float2 lo, float2 hi) { return make_float4(lo.x, lo.y, hi.x, hi.y); }
+__device__ __forceinline__ float2 lo2(float4 a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ float2 hi2(float4 a) { return make_float2(a.z, a.w); }
+__device__ __forceinline__ float4 cadd(float4 a, float4 b) { return f4(cadd(lo2(a), lo2(b)), cadd(hi2(a), hi2(b))); }
+__device__ __forceinline__ float4 csub(float4 a, float4 b) { return f4(csub(lo2(a), lo2(b)), csub(hi2(a), hi2(b))); }
+__device__ __forceinline__ float4 cmul(float4 a, float2 w) { return f4(cmul(lo2(a), w), cmul(hi2(a), w)); }
 __device__ __forceinline__ float4 cmul(float4 a, float4 w) {  // a different weight per line
-    return make_float4(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x), fmaf(a.z, w.z, -a.w * w.w),
-                       fmaf(a.z, w.w, a.w * w.z));
+    return f4(cmul(lo2(a), lo2(w)), cmul(hi2(a), hi2(w)));
 }
 template <typename V> struct RealOf;
 template <> struct RealOf<double2> { using type = double; };
@@ -848,10 +882,16 @@ __global__ void __launch_bounds__(256, 2) pass_kernel_pair(const KArgs a) {
     tile_pair<LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<double2 *>(smem_raw), threadIdx.x);
 }
 
+// (complex128 radix-32 kernels: at most 256 threads, so 255 registers -- a cap of
+// 168 for three CTAs per SM spills and measured slower, profiles/r1_s7_radix32.txt;
+// complex64 ones fit 512 threads at 128 registers: 16-line tiles, 128-byte runs;
+// complex64 lines of <= 256 points keep two 512-thread CTAs per SM)
+template <typename V, int LR> constexpr int pass_min_blocks() {  // 2 CTAs of 512 threads: <= 64 registers
+    return (std::is_same<V, float2>::value && lp_of<V, LR>() <= 4) ? 2 : 1;
+}
 template <typename V, int LR>
-// (radix-32 kernels: at most 256 threads, so 255 registers -- a cap of 168 for
-// three CTAs per SM spills and measured slower, profiles/r1_s7_radix32.txt)
-__global__ void __launch_bounds__(lp_of<V, LR>() == 5 ? 256 : 512) pass_kernel(const KArgs a) {
+__global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512,
+                                  pass_min_blocks<V, LR>()) pass_kernel(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }
@@ -1146,7 +1186,7 @@ __device__ __forceinline__ void decode_tile(const PairArgs &p, int64_t pos, bool
 // fetching its next tile index while it works on the current one, so the
 // queue atomic's latency is hidden.
 template <typename V, int LRA, int LRB>
-__global__ void __launch_bounds__((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5) ? 256 : 512) pair_kernel(const __grid_constant__ PairArgs p) {
+__global__ void __launch_bounds__(((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5) && std::is_same<V, double2>::value) ? 256 : 512) pair_kernel(const __grid_constant__ PairArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t total = p.groups * (p.TA + p.TB);
     // the per-group completion counters only ever grow, by exactly TA / TB per launch

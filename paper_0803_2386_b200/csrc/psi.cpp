@@ -96,7 +96,7 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
     const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
     if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
-    const int64_t max_thr = logP == 5 ? 256 : 512;  // the radix-32 kernels keep 255 registers
+    const int64_t max_thr = (logP == 5 && esize == 16) ? 256 : 512;  // complex128 radix-32 kernels keep 255 registers
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > max_thr || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
@@ -108,7 +108,7 @@ static bool tile_ok(const moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
     const int logR = d.logR, logP = psi_log_p(logR, dtype);
     const int64_t R = int64_t(1) << logR, TPL = R >> logP;
     const int64_t ext0 = d.ndig ? d.ext[0] : 1;
-    return W >= 1 && W * TPL <= (logP == 5 ? 256 : 512) && W * R * esize <= 100 * 1024 && ext0 % W == 0;
+    return W >= 1 && W * TPL <= ((logP == 5 && esize == 16) ? 256 : 512) && W * R * esize <= 100 * 1024 && ext0 % W == 0;
 }
 
 static void set_tile(moa_pass_desc_t &d, moa_dtype_t dtype, int64_t W) {
