@@ -103,8 +103,9 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
  *                        holds X[g + p k2] at offset k2 (the rank is the fastest
  *                        output digit).  A plan may keep natural order (identity
  *                        map) where that costs nothing extra (single-pass plans).
- * Unknown bits -> MOA_EINVAL; LIFTED_ORDER or UNBLOCKED on a 3-D plan, UNBLOCKED
- * with ngpu > 1 or with LIFTED_ORDER -> MOA_EUNSUPPORTED.
+ * Unknown bits -> MOA_EINVAL; LIFTED_ORDER, UNBLOCKED or HYPERCUBE on a 3-D plan,
+ * UNBLOCKED / HYPERCUBE with ngpu > 1, with LIFTED_ORDER or with each other ->
+ * MOA_EUNSUPPORTED.
  */
 #define MOA_FFT_INVERSE 1u
 #define MOA_FFT_NORMALIZE 2u
@@ -115,6 +116,18 @@ moa_status_t moa_fft_plan_3d(moa_fft_plan_t *plan, int64_t n0, int64_t n1, int64
  * global radix-2 stage per pass (t + 1 HBM round trips instead of the
  * lifting's few).  Combines with INVERSE / NORMALIZE, not with LIFTED_ORDER. */
 #define MOA_FFT_UNBLOCKED 8u
+/* MOA_FFT_HYPERCUBE (1-D, ngpu = 1; an ablation, SURVEY §8(f) f3 iii): the
+ * paper's hypercube formulation of the unblocked radix-2 FFT with the stage
+ * transposes t_j of Ch.5 (Eq. tvec; Fig. tvectab)
+ * realised physically: stage s reads its butterfly pairs along the top axis of
+ * the hypercube view, (i, i + n/2) for every i < n/2 -- the same one-loop
+ * control structure at every stage, the "simpler control structure" the paper
+ * conjectures faster -- and stores through the transposition that
+ * brings the next stage's axis to the top (out[(i >> s) 2^{s+1} + (i mod 2^s)
+ * + r 2^s], r = 0, 1; weights w_{2^{s+1}}^{i mod 2^s}).  No input bit reversal
+ * (the transposes sort the output); t HBM round trips, ping-ponging between
+ * out and a plan-owned buffer.  Combines with INVERSE / NORMALIZE only. */
+#define MOA_FFT_HYPERCUBE 16u
 
 /* moa_fft_plan / moa_fft_plan_3d with flags (0 = the forward, natural-order plan). */
 moa_status_t moa_fft_plan_ex(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu,

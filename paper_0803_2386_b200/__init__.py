@@ -15,7 +15,7 @@ _SO = os.path.join(_HERE, "libmoafft.so")
 
 MOA_OK, MOA_EINVAL, MOA_ENOMEM, MOA_ECUDA, MOA_ENCCL, MOA_EUNSUPPORTED = range(6)
 MOA_C64, MOA_C128 = 0, 1
-MOA_FFT_INVERSE, MOA_FFT_NORMALIZE, MOA_FFT_LIFTED_ORDER, MOA_FFT_UNBLOCKED = 1, 2, 4, 8
+MOA_FFT_INVERSE, MOA_FFT_NORMALIZE, MOA_FFT_LIFTED_ORDER, MOA_FFT_UNBLOCKED, MOA_FFT_HYPERCUBE = 1, 2, 4, 8, 16
 MAX_DIGITS = 6
 MAX_PASSES = 36
 STATUS_NAMES = {0: "MOA_OK", 1: "MOA_EINVAL", 2: "MOA_ENOMEM", 3: "MOA_ECUDA", 4: "MOA_ENCCL",
@@ -351,9 +351,10 @@ class FFTPlan:
 
     def __init__(self, n: int = 0, batch: int = 1, dtype="c128", ngpu: int = 1, radices=None, _handle=None,
                  inverse: bool = False, normalize: bool = False, lifted_order: bool = False,
-                 unblocked: bool = False):
+                 unblocked: bool = False, hypercube: bool = False):
         flags = (MOA_FFT_INVERSE if inverse else 0) | (MOA_FFT_NORMALIZE if normalize else 0) | \
-            (MOA_FFT_LIFTED_ORDER if lifted_order else 0) | (MOA_FFT_UNBLOCKED if unblocked else 0)
+            (MOA_FFT_LIFTED_ORDER if lifted_order else 0) | (MOA_FFT_UNBLOCKED if unblocked else 0) | \
+            (MOA_FFT_HYPERCUBE if hypercube else 0)
         if _handle is not None:
             self.h = _handle
         elif radices is not None:

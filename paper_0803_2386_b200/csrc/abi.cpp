@@ -276,7 +276,8 @@ moa_status_t finish_plan(moa_fft_plan_s *p) {
     return build_tables(p);
 }
 
-constexpr uint32_t kAllFlags = MOA_FFT_INVERSE | MOA_FFT_NORMALIZE | MOA_FFT_LIFTED_ORDER | MOA_FFT_UNBLOCKED;
+constexpr uint32_t kAllFlags =
+    MOA_FFT_INVERSE | MOA_FFT_NORMALIZE | MOA_FFT_LIFTED_ORDER | MOA_FFT_UNBLOCKED | MOA_FFT_HYPERCUBE;
 
 // MOA_FFT_UNBLOCKED: P_n (kind 3, in -> out), then t global radix-2 stages in
 // place on out (kind 2, half-distance h = 2^(q-1) in in_kstr, weights w_n^e).
@@ -303,6 +304,30 @@ void unblocked_passes(int64_t n, int64_t batch, std::vector<moa_pass_desc_t> &ou
     }
 }
 
+// MOA_FFT_HYPERCUBE: t stages of kind 4 (stage s in in_kstr = 2^s, ext[0] =
+// rows * n, weights w_n^e), ping-ponging so the last one writes out (1): stage
+// s reads buffer src and writes dst, with dst = out when t - 1 - s is even.
+void hypercube_passes(int64_t n, int64_t batch, std::vector<moa_pass_desc_t> &out) {
+    out.clear();
+    const int t = log2_exact(n);
+    moa_pass_desc_t d;
+    std::memset(&d, 0, sizeof(d));
+    d.kind = 4;
+    d.logR = 1;
+    d.ndig = 1;
+    d.ext[0] = n * batch;
+    d.twN = n;
+    d.out_ksplit = 62;
+    int src = 0;
+    for (int s = 0; s < t; s++) {
+        d.in_kstr = d.out_kstr = int64_t(1) << s;
+        d.src = src;
+        d.dst = ((t - 1 - s) % 2 == 0) ? 1 : 2;
+        out.push_back(d);
+        src = d.dst;
+    }
+}
+
 // MOA_FFT_LIFTED_ORDER on one GPU: the last pass stores each result where it
 // loaded its input (point-contiguous, in place) instead of through the final
 // transpose; the natural descriptor is kept for moa_fft_output_index.
@@ -326,6 +351,9 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
     if (flags & ~kAllFlags) return fail(MOA_EINVAL, "plan: unknown flag bits");
     if ((flags & MOA_FFT_UNBLOCKED) && (ngpu > 1 || (flags & MOA_FFT_LIFTED_ORDER) || radices))
         return fail(MOA_EUNSUPPORTED, "plan: MOA_FFT_UNBLOCKED is one-GPU, natural order, planner-chosen only");
+    if ((flags & MOA_FFT_HYPERCUBE) &&
+        (ngpu > 1 || (flags & (MOA_FFT_LIFTED_ORDER | MOA_FFT_UNBLOCKED)) || radices))
+        return fail(MOA_EUNSUPPORTED, "plan: MOA_FFT_HYPERCUBE is one-GPU, natural order, planner-chosen only");
     if (!pow2(n)) return fail(MOA_EINVAL, "plan: n must be a power of two >= 1 (n = 2^t, t >= 0)");
     if (batch < 1) return fail(MOA_EINVAL, "plan: batch must be >= 1");
     if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan: unknown dtype");
@@ -354,8 +382,10 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
         }
     } else {
         std::vector<int64_t> rad;
-        if (flags & MOA_FFT_UNBLOCKED) {
-            unblocked_passes(n, batch, p->passes);
+        if ((flags & MOA_FFT_UNBLOCKED) || ((flags & MOA_FFT_HYPERCUBE) && n == 1)) {
+            unblocked_passes(n, batch, p->passes);  // (n = 1: the identity copy)
+        } else if (flags & MOA_FFT_HYPERCUBE) {
+            hypercube_passes(n, batch, p->passes);
         } else if (radices) {
             rad.assign(radices, radices + nrad);
         } else {
@@ -363,7 +393,8 @@ moa_status_t plan_1d(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t
             st = parse_lift_env(n, rad, have);
             if (!st && !have) st = plan_radices(n, batch, dtype, rad);
         }
-        if (!st && !(flags & MOA_FFT_UNBLOCKED)) st = psi_build(n, batch, dtype, rad, radices == nullptr, p->passes);
+        if (!st && !(flags & (MOA_FFT_UNBLOCKED | MOA_FFT_HYPERCUBE)))
+            st = psi_build(n, batch, dtype, rad, radices == nullptr, p->passes);
         if (!st && (flags & MOA_FFT_LIFTED_ORDER)) make_lifted_order(p);
     }
     if (!st) st = finish_plan(p);
@@ -410,8 +441,8 @@ moa_status_t moa_fft_plan_3d_ex(moa_fft_plan_t *plan, int64_t n0, int64_t n1, in
     if (!plan) return fail(MOA_EINVAL, "plan_3d: null output pointer");
     *plan = nullptr;
     if (flags & ~kAllFlags) return fail(MOA_EINVAL, "plan_3d: unknown flag bits");
-    if (flags & (MOA_FFT_LIFTED_ORDER | MOA_FFT_UNBLOCKED))
-        return fail(MOA_EUNSUPPORTED, "plan_3d: MOA_FFT_LIFTED_ORDER / MOA_FFT_UNBLOCKED are 1-D only");
+    if (flags & (MOA_FFT_LIFTED_ORDER | MOA_FFT_UNBLOCKED | MOA_FFT_HYPERCUBE))
+        return fail(MOA_EUNSUPPORTED, "plan_3d: MOA_FFT_LIFTED_ORDER / _UNBLOCKED / _HYPERCUBE are 1-D only");
     for (int64_t v : {n0, n1, n2})
         if (!pow2(v) || v > 4096) return fail(MOA_EINVAL, "plan_3d: each extent must be a power of two in [1, 4096]");
     if (dtype != MOA_C64 && dtype != MOA_C128) return fail(MOA_EINVAL, "plan_3d: unknown dtype");

@@ -1410,6 +1410,41 @@ __global__ void __launch_bounds__(256) vl_stage_kernel(V *__restrict__ x, int64_
     }
 }
 
+// One stage of the hypercube form (MOA_FFT_HYPERCUBE, Ch.5): stage s reads the
+// pairs along the top axis of the current hypercube view, (i, i + n/2), and
+// stores through the transposition that brings axis s + 1 to the top --
+// out[(i >> s) 2^{s+1} + j + r 2^s], j = i mod 2^s -- with the weight
+// w_{2^{s+1}}^j = w_n^{j 2^{t-1-s}} on the second element (the radix-2
+// Stockham autosort; the t_j transposes of Eq. tvec P:4991-4993 done physically).
+template <typename V>
+__global__ void __launch_bounds__(256) hyper_stage_kernel(const V *__restrict__ in, V *__restrict__ out,
+                                                          int64_t half_total, int logn, int s,
+                                                          const double2 *__restrict__ hi,
+                                                          const double2 *__restrict__ lo, int twh, int conj_in,
+                                                          int conj_out, double scale) {
+    const int64_t half = int64_t(1) << (logn - 1), ns = int64_t(1) << s;
+    using T = typename RealOf<V>::type;
+    const T sr = T(scale), si = conj_out ? -T(scale) : T(scale);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < half_total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t base = (i >> (logn - 1)) << logn, ii = i & (half - 1);
+        V a = in[base + ii], b = in[base + ii + half];
+        if (conj_in) {
+            a.y = -a.y;
+            b.y = -b.y;
+        }
+        const int64_t j = ii & (ns - 1);
+        const V c = cmul(b, cvt_tw(tw_lookup(hi, lo, j << (logn - 1 - s), twh), V{}));
+        V u = cadd(a, c), v = csub(a, c);
+        if (conj_out || scale != 1.0) {
+            u = mk<V>(u.x * sr, u.y * si);
+            v = mk<V>(v.x * sr, v.y * si);
+        }
+        const int64_t o = base + ((ii >> s) << (s + 1)) + j;
+        out[o] = u;
+        out[o + ns] = v;
+    }
+}
+
 // P_n of every row (Fig. vanloan_fft line 1): out[b n + i] = in[b n + bitrev_t(i)]
 template <typename V>
 __global__ void __launch_bounds__(256) bitrev_kernel(const V *__restrict__ in, V *__restrict__ out, int64_t total, int t,
@@ -1431,11 +1466,17 @@ cudaError_t launch_unblocked(const moa_pass_desc_t &d, const void *in, void *out
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t work = d.kind == 2 ? total / 2 : total;
+    const int64_t work = (d.kind == 2 || d.kind == 4) ? total / 2 : total;
     int64_t grid = (work + 255) / 256;
     if (grid > int64_t(sms) * 16) grid = int64_t(sms) * 16;
     if (grid < 1) grid = 1;
-    if (d.kind == 3) {
+    if (d.kind == 4) {
+        const int lN = log2_exact(d.twN);
+        hyper_stage_kernel<V><<<unsigned(grid), 256, 0, stream>>>(
+            static_cast<const V *>(in), static_cast<V *>(out), work, lN, log2_exact(d.in_kstr),
+            static_cast<const double2 *>(tb.tw_hi), static_cast<const double2 *>(tb.tw_lo), (lN + 1) / 2, mods.conj_in,
+            mods.conj_out, mods.scale);
+    } else if (d.kind == 3) {
         bitrev_kernel<V><<<unsigned(grid), 256, 0, stream>>>(static_cast<const V *>(in), static_cast<V *>(out), total,
                                                               log2_exact(d.twN), mods.conj_in, mods.conj_out, mods.scale);
     } else {
@@ -1826,7 +1867,7 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
 
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
                         cudaStream_t stream, const PassMods &mods) {
-    if (d.kind == 2 || d.kind == 3) {  // the unblocked control: total elements = ext[0] (rows * n)
+    if (d.kind == 2 || d.kind == 3 || d.kind == 4) {  // unblocked control / hypercube: total = ext[0] (rows * n)
         const int64_t total = d.ndig ? d.ext[0] : 1;
         if (dtype == MOA_C128) return launch_unblocked<double2>(d, in, out, tab, stream, mods, total);
         return launch_unblocked<float2>(d, in, out, tab, stream, mods, total);

@@ -58,7 +58,11 @@ def test_other_argument_errors():
         m.moa_psi_describe(64, 1, "c128", [8, 3, 3])
     assert m.lib.moa_fft_destroy(None) == m.MOA_OK
     # plan flags: unknown bits, lifted order on a 3-D plan
-    assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 1, 16) == m.MOA_EINVAL
+    assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 1, 32) == m.MOA_EINVAL
+    for bad in (m.MOA_FFT_HYPERCUBE | m.MOA_FFT_UNBLOCKED, m.MOA_FFT_HYPERCUBE | m.MOA_FFT_LIFTED_ORDER):
+        assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 1, bad) == m.MOA_EUNSUPPORTED
+    assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 2, m.MOA_FFT_HYPERCUBE) == m.MOA_EUNSUPPORTED
+    assert m.lib.moa_fft_plan_3d_ex(ctypes.byref(h), 8, 8, 8, 1, 1, m.MOA_FFT_HYPERCUBE) == m.MOA_EUNSUPPORTED
     assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 2, m.MOA_FFT_UNBLOCKED) == m.MOA_EUNSUPPORTED
     assert m.lib.moa_fft_plan_ex(ctypes.byref(h), 1024, 1, 1, 1,
                                  m.MOA_FFT_UNBLOCKED | m.MOA_FFT_LIFTED_ORDER) == m.MOA_EUNSUPPORTED

@@ -150,3 +150,26 @@ def test_unblocked_control(m, torch_cuda, dtype, n, batch):
     inv = m.FFTPlan(n, batch, dtype, unblocked=True, inverse=True, normalize=True)
     z = run(torch_cuda, inv, x).astype(np.complex128)
     assert rel_l2(z, oracle.fft_radix2_rows_sign(x.astype(np.complex128), n, +1) / n) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("n,batch", [(1, 3), (2, 5), (8, 3), (1 << 10, 4), (1 << 13, 1), (1 << 17, 2), (1 << 20, 1)])
+def test_hypercube_form(m, torch_cuda, dtype, n, batch):
+    # the Ch.5 hypercube stages with physical t_j transposes
+    # (one loop over (i, i + n/2) per stage, no bit reversal), forward and
+    # inverse-normalised, against the oracle
+    x = synth.fill(n * batch, 36, synth.UNIFORM, dtype)
+    ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+    plan = m.FFTPlan(n, batch, dtype, hypercube=True)
+    d = plan.describe()
+    assert n == 1 or (len(d) == int(np.log2(n)) and all(p["kind"] == 4 for p in d))
+    y = run(torch_cuda, plan, x)
+    assert rel_l2(y.astype(np.complex128), ref) <= TOL[dtype]
+    inv = m.FFTPlan(n, batch, dtype, hypercube=True, inverse=True, normalize=True)
+    yi = run(torch_cuda, inv, x)
+    refi = oracle.fft_radix2_rows_sign(x.astype(np.complex128), n, +1) / n
+    assert rel_l2(yi.astype(np.complex128), refi) <= TOL[dtype]
+    xt = torch_cuda.from_numpy(x).cuda()                                   # in == out: staged input
+    plan.exec(xt, xt)
+    torch_cuda.cuda.synchronize()
+    assert rel_l2(xt.cpu().numpy().astype(np.complex128), ref) <= TOL[dtype]

@@ -6,6 +6,10 @@ For n = 2^t (complex128, one transform, inputs resident in HBM) time
   * the planner's lifting (each pass one HBM round trip of <= 2^8-point blocks),
   * the unblocked control: the all-radix-2 lifting, one global radix-2 stage
     per pass (t passes) -- the Van Loan loop with no blocking,
+  * the hypercube form (MOA_FFT_HYPERCUBE): the same t radix-2 stages with the
+    Ch.5 stage transposes t_j done physically, one loop over (i, i + n/2) at
+    every stage -- the paper's "simpler control structure" conjecture
+    (P:5880-5887), which it never measured,
 with CUDA events (median of reps, L2 flushed before each rep), and print one
 JSON line per n.
 """
@@ -48,10 +52,15 @@ def main():
         unb = m.FFTPlan(n, 1, "c128", unblocked=True)
         ms_u = time_plan(unb, x, y)
         unb.close()
+        hyp = m.FFTPlan(n, 1, "c128", hypercube=True)
+        ms_h = time_plan(hyp, x, y)
+        hyp.close()
         gf = lambda ms: 5.0 * n * t / (ms * 1e-3) / 1e9
         print(json.dumps({"n": n, "lifted_radices": rad_l, "lifted_ms": round(ms_l, 4), "lifted_gflops": round(gf(ms_l), 1),
                           "unblocked_passes": t, "unblocked_ms": round(ms_u, 4),
-                          "unblocked_gflops": round(gf(ms_u), 1), "speedup": round(ms_u / ms_l, 2)}), flush=True)
+                          "unblocked_gflops": round(gf(ms_u), 1), "speedup": round(ms_u / ms_l, 2),
+                          "hypercube_ms": round(ms_h, 4), "hypercube_gflops": round(gf(ms_h), 1),
+                          "hypercube_vs_unblocked": round(ms_u / ms_h, 3)}), flush=True)
 
 
 if __name__ == "__main__":
