@@ -207,7 +207,12 @@ template <typename V, int LR> __host__ __device__ constexpr int lp_of() {
                                                                                             : (LR < 4 ? LR : 4);
 }
 
-struct KArgs {
+struct alignas(64) KArgs {
+    // line-fast L2 prefetch (MOA_FFT_PF_LF): tensor map of the load side, boxes
+    // of W lines x 256 points -- one prefetch instruction per box instead of one
+    // per 128-byte run
+    CUtensorMap pf_tmap;
+    int32_t pf_rank, pf_nbox, pf_box_pts, pf_ext0;
     const void *in;
     void *out;
     int64_t in_str[kMaxDigits], out_str[kMaxDigits], tw_str[kMaxDigits];
@@ -638,6 +643,42 @@ __device__ __forceinline__ void prefetch_tile(const KArgs &a, int64_t line0) {
     }
 }
 
+// Tensor-map L2 prefetch of box b of the tile starting at line `line0`
+// (coordinates: 2 digit0 reals, point, digits 1..).
+__device__ __forceinline__ void prefetch_tile_tensor(const KArgs &a, int64_t line0, int b) {
+    int32_t c[5] = {0, 0, 0, 0, 0};
+    int64_t rest = line0;
+    c[0] = int32_t(2 * (rest % a.pf_ext0));
+    rest /= a.pf_ext0;
+    for (int i = 1; i < a.ndig && i + 1 < 5; i++) {
+        c[i + 1] = int32_t(rest & ((int64_t(1) << a.lext[i]) - 1));
+        rest >>= a.lext[i];
+    }
+    c[1] = b * a.pf_box_pts;
+    const uint64_t t = reinterpret_cast<uint64_t>(&a.pf_tmap);
+    switch (a.pf_rank) {
+        case 2:
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(t), "r"(c[0]), "r"(c[1])
+                         : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(t), "r"(c[0]),
+                         "r"(c[1]), "r"(c[2])
+                         : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(t), "r"(c[0]),
+                         "r"(c[1]), "r"(c[2]), "r"(c[3])
+                         : "memory");
+            break;
+        default:
+            asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(t),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+                         : "memory");
+            break;
+    }
+}
+
 // One tile with direct (register) loads -- the non-pipelined form.
 template <typename V, int LR>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
@@ -647,7 +688,13 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     constexpr int LPL = lines_per_lane<V>();
     if (a.pf_dist) {
         const int64_t nt = int64_t(blockIdx.x) + a.pf_dist;
-        if (nt < a.ntiles) prefetch_tile<V, LR>(a, nt * a.W * LPL);
+        if (nt < a.ntiles) {
+            if (a.pf_rank) {
+                if (threadIdx.x < a.pf_nbox) prefetch_tile_tensor(a, nt * a.W * LPL, threadIdx.x);
+            } else {
+                prefetch_tile<V, LR>(a, nt * a.W * LPL);
+            }
+        }
     }
     const TileMap mp = tile_map<TPL>(a, threadIdx.x);
     int64_t b_io, b_oo, b_te;
@@ -898,7 +945,7 @@ template <typename V, int LR> constexpr int pass_min_blocks() {  // 2 CTAs of 51
 }
 template <typename V, int LR>
 __global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512,
-                                  pass_min_blocks<V, LR>()) pass_kernel(const KArgs a) {
+                                  pass_min_blocks<V, LR>()) pass_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }
@@ -1582,6 +1629,21 @@ void set_prefetch(KArgs &a, const void *fn, int threads, int smem, int64_t tiles
     a.ntiles = tiles;
 }
 
+bool encode_lf_tmap(CUtensorMap *map, const moa_pass_desc_t &d, const void *in, int esize, int64_t W, int *rank,
+                    int *nbox, int *box_pts);
+
+// the line-fast side's tensor map for the box prefetch (false: not expressible)
+bool set_lf_prefetch_map(KArgs &a, const moa_pass_desc_t &d, int esize) {
+    int rank = 0, nbox = 0, bp = 0;
+    if (!d.lf_load || d.ndig < 1 || d.in_str[0] != 1 || d.ndig > 4) return false;
+    if (!encode_lf_tmap(&a.pf_tmap, d, a.in, esize, d.W, &rank, &nbox, &bp)) return false;
+    a.pf_rank = rank;
+    a.pf_nbox = nbox;
+    a.pf_box_pts = bp;
+    a.pf_ext0 = int32_t(d.ext[0]);
+    return true;
+}
+
 // ---- warp-specialised launch (MOA_FFT_WS != 0): eligible passes only, else
 // cudaErrorNotSupported and the plain kernel runs
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -1599,6 +1661,41 @@ EncodeTiledFn encode_tiled() {
         return reinterpret_cast<EncodeTiledFn>(p);
     }();
     return fn;
+}
+
+// Tensor map of a line-fast load side (digit 0 = adjacent lines, unit stride):
+// dims (2 digit-0 reals, the R points at in_kstr, line digits 1..), boxes of
+// W lines x min(R, 256) points.
+bool encode_lf_tmap(CUtensorMap *map, const moa_pass_desc_t &d, const void *in, int esize, int64_t W, int *rank_out,
+                    int *nbox, int *box_pts) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const int64_t R = int64_t(1) << d.logR;
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    int rank = 0;
+    dims[rank] = cuuint64_t(2 * d.ext[0]);
+    box[rank++] = cuuint32_t(2 * W);
+    const int64_t bp = R < 256 ? R : 256;
+    dims[rank] = cuuint64_t(R);
+    strides[rank - 1] = cuuint64_t(d.in_kstr * esize);
+    box[rank++] = cuuint32_t(bp);
+    for (int i = 1; i < d.ndig; i++) {
+        dims[rank] = cuuint64_t(d.ext[i]);
+        strides[rank - 1] = cuuint64_t(d.in_str[i] * esize);
+        box[rank++] = 1;
+    }
+    if (2 * W > 256 || (W * esize) % 16) return false;
+    for (int i = 0; i < rank - 1; i++)
+        if (strides[i] % 16 || strides[i] >= (cuuint64_t(1) << 40)) return false;
+    CUresult r = enc(map, esize == 16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     cuuint32_t(rank), const_cast<void *>(in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    *rank_out = rank;
+    *nbox = int(R / bp);
+    *box_pts = int(bp);
+    return true;
 }
 
 int ws_mode() {  // MOA_FFT_WS: 0 off, 1 on (eligible passes)
@@ -1652,32 +1749,11 @@ cudaError_t launch_ws(const std::array<void (*)(const WsArgs), 13> &tab, const m
     if (S < 2) return cudaErrorNotSupported;
     w.stages = S;
     if (mode == 0) {
-        EncodeTiledFn enc = encode_tiled();
-        if (!enc) return cudaErrorNotSupported;
-        cuuint64_t dims[5], strides[4];
-        cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-        int rank = 0;
-        dims[rank] = cuuint64_t(2 * d.ext[0]);
-        box[rank++] = cuuint32_t(2 * d.W);
-        const int64_t bp = R < 256 ? R : 256;
-        dims[rank] = cuuint64_t(R);
-        strides[rank - 1] = cuuint64_t(d.in_kstr * esize);
-        box[rank++] = cuuint32_t(bp);
-        for (int i = 1; i < d.ndig; i++) {
-            dims[rank] = cuuint64_t(d.ext[i]);
-            strides[rank - 1] = cuuint64_t(d.in_str[i] * esize);
-            box[rank++] = 1;
-        }
-        for (int i = 0; i < rank - 1; i++)
-            if (strides[i] % 16 || strides[i] >= (cuuint64_t(1) << 40)) return cudaErrorNotSupported;
-        CUresult r = enc(&w.tmap, esize == 16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                         cuuint32_t(rank), const_cast<void *>(a.in), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return cudaErrorNotSupported;
+        int rank = 0, nbox = 0, bp = 0;
+        if (!encode_lf_tmap(&w.tmap, d, a.in, esize, d.W, &rank, &nbox, &bp)) return cudaErrorNotSupported;
         w.tmap_rank = rank;
-        w.nbox = int32_t(R / bp);
-        w.box_pts = int32_t(bp);
+        w.nbox = nbox;
+        w.box_pts = bp;
         w.ext0 = int32_t(d.ext[0]);
     }
     auto fn = tab[d.logR];
@@ -1701,14 +1777,21 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     const int64_t tiles = nlines / d.W;
     // MOA_FFT_PF = f: prefetch the tile f * (resident CTAs) ahead into L2 (0: off),
     // for contiguous-line (point-fast) loads -- a few large bulk prefetches per
-    // tile.  Line-fast loads would need one 128-byte prefetch per point, which
-    // measured slower (cfg3 4.95 -> 5.8 ms, cfg4 12.0 -> 13.4 ms,
-    // profiles/r2b_ab_pf.jsonl); MOA_FFT_PF_LF = f enables them (ablation).
+    // tile.  Line-fast loads (MOA_FFT_PF_LF = f): one tensor-map box prefetch
+    // (W lines x 256 points) per box (one 128-byte bulk prefetch per point
+    // measured slower: cfg3 4.95 -> 5.8 ms, cfg4 12.0 -> 13.4 ms,
+    // profiles/r2b_ab_pf.jsonl).
     // Default: 0.5 for contiguous lines of >= 512 points (measured: cfg5 passes
     // 6.35 -> 6.22 ms, cfg3's 1024-point last pass 1.71 -> 1.57 ms; cfg2's
     // 256-point rows 0.311 -> 0.315 ms, so not there -- profiles/r2c_ab_cfg5.jsonl,
     // r2b_ab_pf.jsonl).
-    double pf = (!d.lf_load && d.logR >= 9) ? 0.5 : 0.0;
+    // Line-fast loads: default 0.5 when the points are < 1 MiB apart (box
+    // prefetch measured: cfg3 pass 1 (16 KiB) 1.50 -> 1.37 ms, cfg4 pass 2
+    // (2 KiB) 2.90 -> 2.68 ms, cfg2 pass 0 0.341 -> 0.326 ms; but cfg3 pass 0
+    // (8 MiB apart: every box row a different DRAM page) 1.78 -> 2.20 ms,
+    // profiles/r3a_pflf.jsonl).
+    const int64_t kload_b = d.in_kstr * int64_t(sizeof(typename ElemOf<V>::type));
+    double pf = (!d.lf_load && d.logR >= 9) ? 0.5 : (d.lf_load && kload_b < (int64_t(1) << 20)) ? 0.5 : 0.0;
     if (const char *pe = std::getenv(d.lf_load ? "MOA_FFT_PF_LF" : "MOA_FFT_PF")) pf = std::atof(pe);
     // complex64 passes of >= 2^10-point lines coalesced along the lines on both
     // sides (digit 0 unit stride in and out, even tile width): two adjacent
@@ -1761,7 +1844,8 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                 cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
                 if (e != cudaSuccess) return e;
             }
-            if (pf > 0 && !d.ring) set_prefetch(b, reinterpret_cast<const void *>(f), d.threads / 2, d.smem_bytes, tiles, pf);
+            if (pf > 0 && !d.ring && (!d.lf_load || set_lf_prefetch_map(b, d, int(sizeof(float2)))))
+                set_prefetch(b, reinterpret_cast<const void *>(f), d.threads / 2, d.smem_bytes, tiles, pf);
             f<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads / 2)), size_t(d.smem_bytes), stream>>>(b);
             return cudaGetLastError();
         }
@@ -1819,7 +1903,8 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
         if (e != cudaSuccess) return e;
     }
-    if (pf > 0 && !d.ring) set_prefetch(a, reinterpret_cast<const void *>(fn), d.threads, d.smem_bytes, tiles, pf);
+    if (pf > 0 && !d.ring && (!d.lf_load || set_lf_prefetch_map(a, d, int(sizeof(typename ElemOf<V>::type)))))
+        set_prefetch(a, reinterpret_cast<const void *>(fn), d.threads, d.smem_bytes, tiles, pf);
     fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
     return cudaGetLastError();
 }

@@ -86,6 +86,13 @@ cases = [
     ("3-D classic", lambda: three((16, 32, 64), "c128", "0")),
     ("3-D rot", lambda: three((16, 32, 64), "c128", "2")),
     ("3-D c64", lambda: three((32, 16, 64), "c64", "0")),
+    ("small kernel c128", lambda: one(1 << 10, 3, "c128")),
+    ("small kernel c64 odd", lambda: one(1 << 11, 2, "c64")),
+    ("TMA-fed line-fast", lambda: one(1 << 18, 2, "c128", env={"MOA_FFT_WS": "1"}, radices=[512, 512])),
+    ("TMA-fed contiguous", lambda: one(1 << 20, 1, "c128", env={"MOA_FFT_WS": "1"}, radices=[1024, 1024])),
+    ("pair radix-32 c128", lambda: one(1 << 19, 2, "c128", env={"MOA_FFT_PAIR": "1"}, radices=[512, 1024])),
+    ("FP32x2 radix-32 c64", lambda: one(1 << 20, 1, "c64", radices=[1024, 1024])),
+    ("hypercube", lambda: one(1 << 12, 2, "c128", hypercube=True)),
     ("dist fused p4", lambda: dist(1 << 14, 4, "1")),
     ("dist nccl-style p4", lambda: dist(1 << 14, 4, "0")),
 ]
