@@ -91,8 +91,12 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // (only a strided LOAD side needs the long runs: strided stores are merged
     // into full lines in L2 -- tools/stride_bench, the rotating 3-D layouts)
     const int64_t kload = d.in_kstr * esize;
+    // complex64 radix-32 passes loading contiguous lines and storing transposed:
+    // 16-line tiles too (128-byte store runs at one 512-thread CTA per SM;
+    // measured cfg4's 1024^3 last pass 3.54 -> 3.20 ms, profiles/r3c_c64.jsonl)
+    const bool c64_wide = esize == 8 && logP == 5 && !d.lf_load && d.lf_store;
     const int64_t smem_cap = cap_env ? std::atoll(cap_env)
-                                     : (d.lf_load && kload >= (int64_t(1) << 20) ? 200000 : 100 * 1024);
+                                     : ((d.lf_load && kload >= (int64_t(1) << 20)) || c64_wide ? 200000 : 100 * 1024);
     // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
     const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
     if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
@@ -455,12 +459,17 @@ static int fuse_two(std::vector<moa_pass_desc_t> &passes, size_t i, moa_dtype_t 
     if (A.dst != B.src || A.dst < 0) return 0;
     if (G * esize * 4 > ring_budget) return 0;
     if (A.logR < 5 || A.logR > 10 || B.logR < 5 || B.logR > 10) return 0;
-    if (A.threads != B.threads) {  // equalise the CTA size by widening the narrower tile
+    if (A.threads != B.threads) {  // equalise the CTA size: widen the narrower tile, else narrow the wider
         moa_pass_desc_t &lo = A.threads < B.threads ? A : B;
-        const moa_pass_desc_t &hi = A.threads < B.threads ? B : A;
+        moa_pass_desc_t &hi = A.threads < B.threads ? B : A;
         const int64_t W = int64_t(lo.W) * hi.threads / lo.threads;
-        if (!tile_ok(lo, dtype, W)) return 0;
-        set_tile(lo, dtype, W);
+        if (tile_ok(lo, dtype, W)) {
+            set_tile(lo, dtype, W);
+        } else {
+            const int64_t Wh = int64_t(hi.W) * lo.threads / hi.threads;
+            if (Wh < 1 || !tile_ok(hi, dtype, Wh)) return 0;
+            set_tile(hi, dtype, Wh);
+        }
         if (A.threads != B.threads) return 0;
     }
     const char *mb = std::getenv("MOA_FFT_RING_MB");  // ablation: ring size budget
@@ -669,6 +678,13 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
     // L2 pairs (MOA_FFT_LIFT4) need the four factors.
     const char *l4env = std::getenv("MOA_FFT_LIFT4");
     const bool lift4 = l4env && l4env[0] == '1';
+    // complex64 2^30 (cfg4): three 1024-point passes since the packed FP32x2
+    // arithmetic and the 16-line tiles (11.1-11.3 ms against 11.7 ms for the
+    // four-pass (256, 128, 128, 256), profiles/r3c_c64.jsonl, r3d_c64.jsonl)
+    if (!lift4 && dtype == MOA_C64 && t == 30) {
+        for (int k = 0; k < 3; k++) radices.push_back(int64_t(1) << 10);
+        return MOA_OK;
+    }
     if (t >= (lift4 ? 26 : 30) && t % 2 == 0 && t <= 32) {
         const int a = (t + 3) / 4, b = t / 2 - a;
         for (int x : {a, b, b, a}) radices.push_back(int64_t(1) << x);

@@ -75,7 +75,7 @@ def test_planner_liftings():
     assert m.moa_plan_radices(1 << 16) == [256, 256]
     assert m.moa_plan_radices(1 << 28, 1, "c128") == [512, 512, 1024]        # radix-32 lines: 3 passes
     assert m.moa_plan_radices(1 << 26, 1, "c64") == [256, 512, 512]
-    assert m.moa_plan_radices(1 << 30, 1, "c64") == [256, 128, 128, 256]
+    assert m.moa_plan_radices(1 << 30, 1, "c64") == [1024, 1024, 1024]       # FP32x2 radix-32: 3 passes
     r3 = m.moa_plan_radices(1 << 27, 1, "c128")                              # odd t: three passes
     assert np.prod(r3) == 1 << 27 and len(r3) == 3 and max(r3[:-1]) <= 512
     for t in range(0, 34):
@@ -88,10 +88,15 @@ def test_bench_config_tiles():
     # cfg2 two 256-point passes, 16-line tiles (256-byte runs)
     d2 = m.moa_psi_describe(1 << 16, 1024, "c128")
     assert [(1 << d["logR"], d["W"], d["threads"]) for d in d2] == [(256, 16, 256), (256, 16, 256)]
-    # cfg4: the first pass loads 32 MiB apart -> 32 lines (256-byte runs of complex64)
+    # cfg4: three 1024-point complex64 passes (radix 32 x 32 on the FP32x2 pipe);
+    # 16-line tiles (128-byte runs) where the loads are >= 1 MiB apart and where
+    # contiguous lines are stored transposed; 8 lines for the 8 KiB-strided middle pass
     d4 = m.moa_psi_describe(1 << 30, 1, "c64")
-    assert [1 << d["logR"] for d in d4] == [256, 128, 128, 256]
-    assert d4[0]["W"] == 32 and d4[0]["threads"] == 512 and d4[1]["W"] == 16
+    assert [1 << d["logR"] for d in d4] == [1024, 1024, 1024]
+    assert [d["W"] for d in d4] == [16, 8, 16] and [d["threads"] for d in d4] == [512, 256, 512]
+    # the four-factor lifting it replaced: the 32 MiB-strided first pass takes 32 lines
+    d4b = m.moa_psi_describe(1 << 30, 1, "c64", [256, 128, 128, 256])
+    assert d4b[0]["W"] == 32 and d4b[0]["threads"] == 512 and d4b[1]["W"] == 16
     # cfg5: complex128 1024-point lines take 32 points per thread (radix 32 x 32; 512-point lines too)
     for d in m.moa_psi_describe_3d(1024, 1024, 1024, "c128"):
         assert d["logR"] == 10 and d["W"] * 32 == d["threads"] and d["threads"] <= 256
