@@ -541,6 +541,9 @@ def main():
     dist = world > 1
     td = None
     if dist:
+        # NCCL's INFO init lines (communicator rank counts) stay visible to the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as td
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
     subs = [] if args.no_sub_configs else (
