@@ -12,6 +12,10 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libmoafft.so")
+# A/B measurements only: MOA_FFT_LIB_AB names another in-tree build of the
+# same library (e.g. paper_0803_2386_b200/build/ab/libmoafft_prev.so)
+if os.environ.get("MOA_FFT_LIB_AB"):
+    _SO = os.path.join(os.path.dirname(_HERE), os.environ["MOA_FFT_LIB_AB"])
 
 MOA_OK, MOA_EINVAL, MOA_ENOMEM, MOA_ECUDA, MOA_ENCCL, MOA_EUNSUPPORTED = range(6)
 MOA_C64, MOA_C128 = 0, 1

@@ -1127,7 +1127,8 @@ __global__ void __launch_bounds__(2 * kWsGroupMax, 1) ws_pass_kernel(const __gri
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     const KArgs &a = w.a;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_ws[];
+    unsigned char *smem_raw = smem_ws;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
     int64_t *tile_of = reinterpret_cast<int64_t *>(full + kWsStagesMax);  // [stage][tile, k]
     V *stage0 = reinterpret_cast<V *>(smem_raw + 128);
@@ -1864,10 +1865,12 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             const size_t smem = (2 * size_t(R + (R >> 4)) + size_t(3 * R / 4)) * sizeof(V);
             KFn<V> fn = small[d.logR - 6];
             static std::mutex mu;
-            static std::map<const void *, size_t> attr;  // opt-in shared memory set once per kernel
+            static std::map<std::pair<int, const void *>, size_t> attr;  // opt-in smem set once per (device, kernel)
             if (smem > 48 * 1024) {
+                int dev = 0;
+                cudaGetDevice(&dev);
                 std::lock_guard<std::mutex> g(mu);
-                size_t &have = attr[reinterpret_cast<const void *>(fn)];
+                size_t &have = attr[{dev, reinterpret_cast<const void *>(fn)}];
                 if (have < smem) {
                     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
                     if (e != cudaSuccess) return e;
