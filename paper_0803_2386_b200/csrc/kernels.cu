@@ -931,7 +931,7 @@ __device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2
 }
 
 template <int LR>
-__global__ void __launch_bounds__(256, 2) pass_kernel_pair(const KArgs a) {
+__global__ void __launch_bounds__(512, 1) pass_kernel_pair(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_pair<LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<double2 *>(smem_raw), threadIdx.x);
 }
@@ -1886,7 +1886,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     if constexpr (std::is_same<V, double2>::value) {
         const char *pe = std::getenv("MOA_FFT_PAIR");
         if (pe && pe[0] == '1' && (d.logR == 9 || d.logR == 10) && d.kind == 0 && !d.ring && !mods.npeers &&
-            2 * d.threads <= 256) {
+            2 * d.threads <= 512) {
             auto fn = d.logR == 9 ? &pass_kernel_pair<9> : &pass_kernel_pair<10>;
             if (d.smem_bytes > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
