@@ -685,6 +685,26 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
         for (int k = 0; k < 3; k++) radices.push_back(int64_t(1) << 10);
         return MOA_OK;
     }
+    // The paper chooses its blocking size c by measurement; so does
+    // this planner where a sweep of every 2-4-factor lifting of one transform
+    // beat the rules below (profiles/r3l_planner.jsonl, one B200): complex128
+    // prefers a contiguous 1024-point last pass (2^20 0.0274 -> 0.0241 ms, 2^24
+    // 0.272 -> 0.268, 2^27 2.26 -> 2.13, 2^29 12.1 -> 10.1, 2^30 23.0 -> 22.3 ms);
+    // complex64 two passes at 2^20 / 2^21 and the larger radix first at 2^25 / 2^26.
+    if (!lift4) {
+        static const int c128_tab[][4] = {{20, 10, 10, 0}, {21, 10, 11, 0}, {24, 7, 7, 10},   {25, 7, 8, 10},
+                                          {26, 8, 8, 10},  {27, 8, 9, 10},  {28, 9, 9, 10},   {29, 9, 10, 10},
+                                          {30, 10, 10, 10}};
+        static const int c64_tab[][4] = {{20, 9, 11, 0}, {21, 10, 11, 0}, {25, 9, 8, 8}, {26, 9, 8, 9}};
+        const int(*tab)[4] = dtype == MOA_C128 ? c128_tab : c64_tab;
+        const int cnt = dtype == MOA_C128 ? 9 : 4;
+        for (int i = 0; i < cnt; i++)
+            if (tab[i][0] == t) {
+                for (int k = 1; k < 4; k++)
+                    if (tab[i][k]) radices.push_back(int64_t(1) << tab[i][k]);
+                return MOA_OK;
+            }
+    }
     if (t >= (lift4 ? 26 : 30) && t % 2 == 0 && t <= 32) {
         const int a = (t + 3) / 4, b = t / 2 - a;
         for (int x : {a, b, b, a}) radices.push_back(int64_t(1) << x);

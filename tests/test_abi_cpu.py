@@ -74,10 +74,16 @@ def test_planner_liftings():
     assert m.moa_plan_radices(1 << 10) == [1 << 10]
     assert m.moa_plan_radices(1 << 16) == [256, 256]
     assert m.moa_plan_radices(1 << 28, 1, "c128") == [512, 512, 1024]        # radix-32 lines: 3 passes
-    assert m.moa_plan_radices(1 << 26, 1, "c64") == [256, 512, 512]
+    assert m.moa_plan_radices(1 << 26, 1, "c64") == [512, 256, 512]          # measured table (r3l_planner)
     assert m.moa_plan_radices(1 << 30, 1, "c64") == [1024, 1024, 1024]       # FP32x2 radix-32: 3 passes
+    assert m.moa_plan_radices(1 << 20, 1, "c128") == [1024, 1024]
+    assert m.moa_plan_radices(1 << 29, 1, "c128") == [512, 1024, 1024]       # contiguous 1024-point last pass
     r3 = m.moa_plan_radices(1 << 27, 1, "c128")                              # odd t: three passes
-    assert np.prod(r3) == 1 << 27 and len(r3) == 3 and max(r3[:-1]) <= 512
+    assert np.prod(r3) == 1 << 27 and len(r3) == 3 and r3[-1] == 1024
+    for dt in ("c128", "c64"):
+        for t in range(13, 34):                                              # multi-pass: strided lines <= 2^10
+            r = m.moa_plan_radices(1 << t, 1, dt)
+            assert len(r) >= 2 and max(r[:-1]) <= 1024 and r[-1] <= 4096
     for t in range(0, 34):
         r = m.moa_plan_radices(1 << t)
         assert int(np.prod(r)) == 1 << t and all(x <= 4096 for x in r)
