@@ -692,12 +692,15 @@ moa_status_t plan_radices(int64_t n, int64_t batch, moa_dtype_t dtype, std::vect
     // 0.272 -> 0.268, 2^27 2.26 -> 2.13, 2^29 12.1 -> 10.1, 2^30 23.0 -> 22.3 ms);
     // complex64 two passes at 2^20 / 2^21 and the larger radix first at 2^25 / 2^26.
     if (!lift4) {
-        static const int c128_tab[][4] = {{20, 10, 10, 0}, {21, 10, 11, 0}, {24, 7, 7, 10},   {25, 7, 8, 10},
-                                          {26, 8, 8, 10},  {27, 8, 9, 10},  {28, 9, 9, 10},   {29, 9, 10, 10},
-                                          {30, 10, 10, 10}};
-        static const int c64_tab[][4] = {{20, 9, 11, 0}, {21, 10, 11, 0}, {25, 9, 8, 8}, {26, 9, 8, 9}};
+        // (batched rows, 1 GiB of them, r3n_batched.jsonl / r3o_cfg2.jsonl: complex128
+        // 2^18 [256, 1024] -3 %, complex64 2^13 [32, 256] / 2^14 [64, 256] -2.4 / -3.8 %)
+        static const int c128_tab[][4] = {{18, 8, 10, 0}, {20, 10, 10, 0}, {21, 10, 11, 0}, {24, 7, 7, 10},
+                                          {25, 7, 8, 10},  {26, 8, 8, 10},  {27, 8, 9, 10},  {28, 9, 9, 10},
+                                          {29, 9, 10, 10}, {30, 10, 10, 10}};
+        static const int c64_tab[][4] = {{13, 5, 8, 0},  {14, 6, 8, 0}, {20, 9, 11, 0},
+                                         {21, 10, 11, 0}, {25, 9, 8, 8}, {26, 9, 8, 9}};
         const int(*tab)[4] = dtype == MOA_C128 ? c128_tab : c64_tab;
-        const int cnt = dtype == MOA_C128 ? 9 : 4;
+        const int cnt = dtype == MOA_C128 ? 10 : 6;
         for (int i = 0; i < cnt; i++)
             if (tab[i][0] == t) {
                 for (int k = 1; k < 4; k++)

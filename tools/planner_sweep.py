@@ -42,27 +42,29 @@ ap.add_argument("tmin", type=int, nargs="?", default=20)
 ap.add_argument("tmax", type=int, nargs="?", default=28)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dtypes", default="c128,c64")
+ap.add_argument("--total", type=int, default=0, help="batched: rows = 2^total / n (0: one transform)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 for dt in a.dtypes.split(","):
     tdt = torch.complex128 if dt == "c128" else torch.complex64
     for t in range(a.tmin, a.tmax + 1):
         n = 1 << t
-        x = torch.randn(n, dtype=tdt, device="cuda")
+        batch = (1 << a.total) // n if a.total else 1
+        x = torch.randn(n * batch, dtype=tdt, device="cuda")
         y = torch.empty_like(x)
-        planned = m.moa_plan_radices(n, 1, dt)
+        planned = m.moa_plan_radices(n, batch, dt)
         res = []
         for f in liftings(t):
             rad = [1 << v for v in f]
             try:
-                p = m.FFTPlan(n, 1, dt, radices=rad)
+                p = m.FFTPlan(n, batch, dt, radices=rad)
                 res.append((timeit(p, x, y, a.reps), rad))
                 p.close()
             except Exception:
                 pass
         res.sort()
         tp = next((ms for ms, r in res if r == planned), None)
-        print(json.dumps({"dtype": dt, "t": t, "planned": planned, "planned_ms": tp and round(tp, 4),
+        print(json.dumps({"dtype": dt, "t": t, "batch": batch, "planned": planned, "planned_ms": tp and round(tp, 4),
                           "best": res[0][1], "best_ms": round(res[0][0], 4),
                           "planned_rank": next((i for i, (ms, r) in enumerate(res) if r == planned), None),
                           "candidates": len(res), "top5": [(round(ms, 4), r) for ms, r in res[:5]]}), flush=True)
