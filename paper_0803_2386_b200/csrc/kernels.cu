@@ -243,11 +243,6 @@ struct alignas(64) KArgs {
     // the paper's "pre-fetching becomes a deterministic cost"
     int64_t pf_dist, ntiles;
     int32_t twtab;  // MOA_FFT_TWTAB=1: complex128 step twiddles from the table (ablation)
-    // complex64 line-fast sides with adjacent lines: lanes 2q, 2q+1 move 16-byte
-    // pairs (two adjacent lines at one point) and swap halves with a shuffle --
-    // half the global load / store instructions.  Ablation (MOA_FFT_C64V2=1):
-    // measured slower, cfg4 11.10 -> 11.95 ms (profiles/r3p_v2.jsonl)
-    int32_t v2_load, v2_store;
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -606,28 +601,6 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         if (tid == 0) __threadfence_system();
         return;
     }
-    if constexpr (std::is_same<V, float2>::value) {
-        if (a.v2_store) {
-            // lanes (2q, 2q+1) = lines (2q, 2q+1), same points: lane h stores the
-            // 16-byte pair of both lines at point tB + (m + h P/2) TPL, m < P/2
-            const uint64_t pol = l2_policy(false);
-            const int h = lB & 1;
-            float2 *o = out + oo - int64_t(h) * a.out_str[0];  // line 2q
-#pragma unroll
-            for (int m = 0; m < P / 2; m++) {
-                const float2 mine = h ? pts[m + P / 2] : pts[m];   // this lane's line at the stored point
-                const float2 send = h ? pts[m] : pts[m + P / 2];   // the partner's point, this lane's line
-                float2 recv;
-                recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-                recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-                const float4 v = h ? make_float4(recv.x, recv.y, mine.x, mine.y)
-                                   : make_float4(mine.x, mine.y, recv.x, recv.y);
-                const int kk = tB + (m + h * (P / 2)) * TPL;
-                st_pol(reinterpret_cast<float4 *>(o + int64_t(kk) * a.out_kstr), v, pol);
-            }
-            return;
-        }
-    }
     {
         const uint64_t pol = l2_policy(a.ring == 2);
         if (a.ksplit >= LR) {  // the common case: one affine stride per point
@@ -736,34 +709,10 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
         // form costs an add and a scaled add per point)
         const char *ptr = reinterpret_cast<const char *>(reinterpret_cast<const E *>(a.in) + io + int64_t(mp.tA) * a.in_kstr);
         const int64_t stepb = int64_t(TPL) * a.in_kstr * int64_t(sizeof(E));
-        bool done = false;
-        if constexpr (std::is_same<V, float2>::value) {
-            if (a.v2_load) {
-                // lanes (2q, 2q+1) = lines (2q, 2q+1): lane h loads both lines' 16-byte
-                // pair at point tA + (m + h P/2) TPL and swaps halves with its partner
-                const int h = mp.lA & 1;
-                const char *p2 = ptr - int64_t(h) * a.in_str[0] * int64_t(sizeof(E)) + int64_t(h) * (P / 2) * stepb;
 #pragma unroll
-                for (int m = 0; m < P / 2; m++) {
-                    const float4 v = ld_pol(reinterpret_cast<const float4 *>(p2), pol);
-                    p2 += stepb;
-                    const float2 mine = h ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
-                    const float2 send = h ? make_float2(v.x, v.y) : make_float2(v.z, v.w);
-                    float2 recv;
-                    recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-                    recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-                    pts[m] = h ? recv : mine;
-                    pts[m + P / 2] = h ? mine : recv;
-                }
-                done = true;
-            }
-        }
-        if (!done) {
-#pragma unroll
-            for (int m = 0; m < P; m++) {
-                pts[m] = ld_pol(reinterpret_cast<const V *>(ptr), pol);
-                ptr += stepb;
-            }
+        for (int m = 0; m < P; m++) {
+            pts[m] = ld_pol(reinterpret_cast<const V *>(ptr), pol);
+            ptr += stepb;
         }
     }
     if (a.conj_in) {  // inverse transform: DFT of conj(x) (the plan's first pass)
@@ -1653,19 +1602,6 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.lf_store = d.lf_store;
     a.ring = d.ring;
     if (const char *te = std::getenv("MOA_FFT_TWTAB")) a.twtab = te[0] == '1';
-    if (dtype_esize == 8 && !d.ring && d.ndig >= 1 && d.W >= 2 && d.W % 2 == 0) {
-        const char *ve = std::getenv("MOA_FFT_C64V2");
-        if (ve && ve[0] == '1') {
-            // (16-byte alignment of every pair: all other strides even)
-            bool ev_in = d.in_kstr % 2 == 0, ev_out = d.out_kstr % 2 == 0;
-            for (int i = 1; i < d.ndig; i++) {
-                ev_in = ev_in && d.in_str[i] % 2 == 0;
-                ev_out = ev_out && d.out_str[i] % 2 == 0;
-            }
-            a.v2_load = d.lf_load && d.in_str[0] == 1 && ev_in;
-            a.v2_store = d.lf_store && d.out_str[0] == 1 && ev_out && d.out_ksplit >= d.logR && !mods.npeers;
-        }
-    }
     // discard.global.L2 drops whole 128-byte lines: only when every line a
     // consumed 128-byte run touches belongs to this tile (a line-fast side with
     // adjacent lines adjacent in memory and W * esize >= 128, or a point-fast
