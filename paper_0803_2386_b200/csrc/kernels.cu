@@ -242,7 +242,6 @@ struct alignas(64) KArgs {
     // CTAs ahead), so that tile's loads hit L2 instead of waiting on DRAM --
     // the paper's "pre-fetching becomes a deterministic cost"
     int64_t pf_dist, ntiles;
-    int32_t twtab;  // MOA_FFT_TWTAB=1: complex128 step twiddles from the table (ablation)
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -310,7 +309,7 @@ __device__ __forceinline__ void st_pol(float2 *p, float2 v, uint64_t pol) {
 // (j / NS) NS Q + (j mod NS) + r NS (the self-sorting index map).
 template <int LR, int LP, int LQ, int LNS, bool LAST, int LB, typename V>
 __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int t,
-                                              const typename ElemOf<V>::type *__restrict__ twR, bool twtab) {
+                                              const typename ElemOf<V>::type *__restrict__ twR) {
     constexpr int R = 1 << LR, P = 1 << LP, Q = 1 << LQ, NS = 1 << LNS, G = P / Q;
 #pragma unroll
     for (int u = 0; u < G; u++) {
@@ -318,13 +317,7 @@ __device__ __forceinline__ void stockham_step(V (&pts)[1 << LP], V *sm_line, int
         V v[Q];
 #pragma unroll
         for (int r = 0; r < Q; r++) v[r] = pts[u + r * G];
-        if (NS > 1 && Q >= 4 && std::is_same<V, double2>::value && twtab) {
-            // (ablation MOA_FFT_TWTAB=1: complex128 step twiddles loaded from the
-            // step-major table, one load per twiddle, instead of the products below)
-            const int jm = j & (NS - 1);
-#pragma unroll
-            for (int r = 1; r < Q; r++) v[r] = cmul(v[r], __ldg(twR + (r * NS + jm - 1)));
-        } else if constexpr (NS > 1 && Q >= 4 && std::is_same<V, double2>::value) {
+        if constexpr (NS > 1 && Q >= 4 && std::is_same<V, double2>::value) {
             // complex128 step twiddles w^r, w = w_{NS Q}^{jm}: one table load (entry
             // NS + jm - 1 of the step-major table) and the powers as products A[a] B[b]
             // (r = 4a + b, B[b] = w^b, A[a] = w^{4a}; <= 5 factors deep, ~1e-15) --
@@ -390,7 +383,7 @@ struct NoFree {
 template <int LR, int LP, int LB, int S, int NSTEP, typename V, typename Sync, typename OnFree>
 __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int lA, int tA, int lB, int tB,
                                          const typename ElemOf<V>::type *__restrict__ twR, const Sync &sync,
-                                         const OnFree &on_free, bool twtab = false) {
+                                         const OnFree &on_free) {
     // radix P for every step but the last, which takes the remainder (so step 0,
     // whose writes are strided by its radix, always has radix 16)
     constexpr int LQL = LR - LP * (NSTEP - 1);
@@ -398,8 +391,8 @@ __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int l
     constexpr int LQ = S == NSTEP - 1 ? LQL : LP;
     constexpr int LNS = LP * S;
     constexpr bool LAST = S == NSTEP - 1;
-    if constexpr (S == 0) stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lA * LS, tA, twR, twtab);
-    else stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lB * LS, tB, twR, twtab);
+    if constexpr (S == 0) stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lA * LS, tA, twR);
+    else stockham_step<LR, LP, LQ, LNS, LAST, LB>(pts, sm + lB * LS, tB, twR);
     if constexpr (!LAST) {
         sync();
         const V *sl = sm + lB * LS;
@@ -407,7 +400,7 @@ __device__ __forceinline__ void line_fft(V (&pts)[1 << LP], V *sm, int LS, int l
         for (int m = 0; m < P; m++) pts[m] = sl[swz<LB>(tB + m * (R / P))];
         sync();
         if constexpr (S + 1 == NSTEP - 1) on_free(true);  // no shared-memory access after this
-        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm, LS, lA, tA, lB, tB, twR, sync, on_free, twtab);
+        line_fft<LR, LP, LB, S + 1, NSTEP>(pts, sm, LS, lA, tA, lB, tB, twR, sync, on_free);
     }
 }
 
@@ -489,7 +482,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     bool moved = false;
     if constexpr (LR > 0 && NSTEP > 1) {
         if (!a.nodft) {
-            line_fft<LR, LP, LB, 0, NSTEP>(pts, sm, a.LS, lA, tA, lB, tB, twR, sync, on_free, a.twtab != 0);
+            line_fft<LR, LP, LB, 0, NSTEP>(pts, sm, a.LS, lA, tA, lB, tB, twR, sync, on_free);
             moved = true;
         }
     } else if constexpr (LR > 0) {
@@ -1601,7 +1594,6 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.lf_load = d.lf_load;
     a.lf_store = d.lf_store;
     a.ring = d.ring;
-    if (const char *te = std::getenv("MOA_FFT_TWTAB")) a.twtab = te[0] == '1';
     // discard.global.L2 drops whole 128-byte lines: only when every line a
     // consumed 128-byte run touches belongs to this tile (a line-fast side with
     // adjacent lines adjacent in memory and W * esize >= 128, or a point-fast

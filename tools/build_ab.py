@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Build an A/B variant of libmoafft.so whose kernels.cu comes from a git
-revision (the other objects from the working tree), for same-box timing
+revision or a file (the other objects from the working tree), for same-box timing
 against the current build:  build_ab.py REV [NAME]  ->
 paper_0803_2386_b200/build/ab/libmoafft_NAME.so; select it with
 MOA_FFT_LIB_AB=paper_0803_2386_b200/build/ab/libmoafft_NAME.so."""
@@ -21,7 +21,11 @@ out = os.path.join(b.BUILD, "ab")
 os.makedirs(out, exist_ok=True)
 src = os.path.join(out, f"_ab_{name}_kernels.cu")
 with open(src, "w") as f:
-    f.write(subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:paper_0803_2386_b200/csrc/kernels.cu"], text=True))
+    if os.path.exists(rev):  # a file path instead of a git revision
+        f.write(open(rev).read())
+    else:
+        f.write(subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:paper_0803_2386_b200/csrc/kernels.cu"],
+                                        text=True))
 try:
     obj = os.path.join(out, f"kernels_{name}.o")
     subprocess.check_call([b.NVCC] + b._flags() + ["-I" + b.CSRC, "-c", src, "-o", obj])
