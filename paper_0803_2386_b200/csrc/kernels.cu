@@ -433,8 +433,11 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a, i
 // butterflies, lifted weights, store.  ring >= 0: the ring slot of this
 // tile's group (the L2-staged intermediate of a fused pass pair, see
 // pair_kernel); the ring side's address gets slot * ringG added.
+// kFull: the L2-ring (fused pair) and fused-exchange (peer store) paths are
+// compiled in; the plain pass kernel is built without them (their switched-off
+// branches cost the default path ~1 %, profiles/r3s_noopt.jsonl)
 template <typename V, int LR, typename Sync = CtaSync, typename OnFree = NoFree,
-          bool kEarlyTw = std::is_same<V, double2>::value>
+          bool kEarlyTw = std::is_same<V, double2>::value, bool kFull = true>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
                                              V (&pts)[1 << lp_of<V, LR>()], int64_t b_io, int64_t b_oo,
                                              int64_t b_te, int tid, const Sync &sync = Sync(),
@@ -504,7 +507,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     // ---- ring: every thread has consumed its loads (the exchanges above, or the
     //      barrier here); drop the ring lines this tile read from L2 without a
     //      write-back (discard.global.L2): the intermediate never reaches HBM
-    if (LPL == 1 && a.ring == 1 && a.discard) {
+    if (kFull && LPL == 1 && a.ring == 1 && a.discard) {
         sync();
         constexpr int EPL = 128 / int(sizeof(V));  // elements per 128-byte line
         const int64_t io = b_io + int64_t(lA) * a.in_str[0] + ring_off;
@@ -522,7 +525,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     //         in double precision (<= 15 products, ~1e-15 relative)
     // (the W lines of a tile share every digit but digit 0, which W divides)
     int64_t oo = b_oo + int64_t(LPL * lB) * a.out_str[0];
-    if (a.ring == 2) oo += ring_off;
+    if (kFull && a.ring == 2) oo += ring_off;
     if (a.twmask) {
         if constexpr (!kEarlyTw) fetch_tw();
         double2 w = cmul(tq[0][0], tq[0][1]);
@@ -576,7 +579,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     }
 
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
-    if (a.npeers) {  // fused all-to-all: send-layout offset q -> peer q / chunk (NVLink store)
+    if (kFull && a.npeers) {  // fused all-to-all: send-layout offset q -> peer q / chunk (NVLink store)
         const uint64_t pol = l2_policy(false);
         const int64_t cmask = (int64_t(1) << a.log_chunk) - 1;
 #pragma unroll
@@ -595,7 +598,7 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         return;
     }
     {
-        const uint64_t pol = l2_policy(a.ring == 2);
+        const uint64_t pol = l2_policy(kFull && a.ring == 2);
         if (a.ksplit >= LR) {  // the common case: one affine stride per point
             char *ptr = reinterpret_cast<char *>(out + oo + int64_t(tB) * a.out_kstr);
             const int64_t stepb = int64_t(TPL) * a.out_kstr * int64_t(sizeof(E));
@@ -673,7 +676,7 @@ __device__ __forceinline__ void prefetch_tile_tensor(const KArgs &a, int64_t lin
 }
 
 // One tile with direct (register) loads -- the non-pipelined form.
-template <typename V, int LR>
+template <typename V, int LR, bool kFull = true>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
@@ -693,11 +696,11 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
     int64_t b_io, b_oo, b_te;
     line_offsets(a, line0, b_io, b_oo, b_te);  // the tile's first line; line l adds l * str[0]
     int64_t io = b_io + int64_t(LPL * mp.lA) * a.in_str[0];
-    if (a.ring == 1) io += ring_off;
+    if (kFull && a.ring == 1) io += ring_off;
     V pts[P];
     // ---- 1. load (128-bit; streaming from HBM, L2-only from the ring)
     {
-        const uint64_t pol = l2_policy(a.ring == 1);
+        const uint64_t pol = l2_policy(kFull && a.ring == 1);
         // byte-pointer increments: one 64-bit add per point (the element-index
         // form costs an add and a scaled add per point)
         const char *ptr = reinterpret_cast<const char *>(reinterpret_cast<const E *>(a.in) + io + int64_t(mp.tA) * a.in_kstr);
@@ -715,7 +718,8 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
             if constexpr (LPL == 2) pts[m].w = -pts[m].w;
         }
     }
-    tile_compute<V, LR>(a, line0, sm, ring_off, pts, b_io, b_oo, b_te, threadIdx.x);
+    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, kFull>(a, line0, sm, ring_off, pts, b_io, b_oo,
+                                                                              b_te, threadIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -936,11 +940,11 @@ __global__ void __launch_bounds__(512, 1) pass_kernel_pair(const KArgs a) {
 template <typename V, int LR> constexpr int pass_min_blocks() {  // 2 CTAs of 512 threads: <= 64 registers
     return (std::is_same<V, float2>::value && lp_of<V, LR>() <= 4) ? 2 : 1;
 }
-template <typename V, int LR>
+template <typename V, int LR, bool kFull = false>
 __global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512,
                                   pass_min_blocks<V, LR>()) pass_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    tile_body<V, LR>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
+    tile_body<V, LR, kFull>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1543,6 +1547,10 @@ template <typename V> using PFn = void (*)(const PairArgs);
 template <typename V, int... Ls> constexpr auto make_table(std::integer_sequence<int, Ls...>) {
     return std::array<KFn<V>, sizeof...(Ls)>{&pass_kernel<V, Ls>...};
 }
+// the same kernels with the fused-exchange (peer store) path compiled in
+template <typename V, int... Ls> constexpr auto make_full_table(std::integer_sequence<int, Ls...>) {
+    return std::array<KFn<V>, sizeof...(Ls)>{&pass_kernel<V, Ls, true>...};
+}
 // fused pairs: R_A, R_B in 2^5 .. 2^10 (36 instantiations per dtype)
 template <typename V, int... Is> constexpr auto make_pair_table(std::integer_sequence<int, Is...>) {
     return std::array<PFn<V>, sizeof...(Is)>{&pair_kernel<V, 5 + Is / 6, 5 + Is % 6>...};
@@ -1553,6 +1561,8 @@ const std::array<KFn<double2>, 13> kTab128 = make_table<double2>(std::make_integ
 // paired complex64 lines (float4 = two adjacent lines)
 const std::array<KFn<float4>, 13> kTabPair64 = make_table<float4>(std::make_integer_sequence<int, 13>{});
 const std::array<KFn<float2>, 13> kTab64 = make_table<float2>(std::make_integer_sequence<int, 13>{});
+const std::array<KFn<double2>, 13> kTabFull128 = make_full_table<double2>(std::make_integer_sequence<int, 13>{});
+const std::array<KFn<float2>, 13> kTabFull64 = make_full_table<float2>(std::make_integer_sequence<int, 13>{});
 
 KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTables &tb, int64_t *nlines,
                 const PassMods &mods, int dtype_esize) {
@@ -1797,7 +1807,8 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
             return pe && pe[0] == '0' ? 0 : pe && pe[0] == '1' ? 2 : 1;
         }();
         const int min_lr = pair_mode == 2 ? 4 : 10;
-        if (pair_mode && psi_log_p(d.logR, MOA_C64) == 4 && d.lf_load && d.lf_store && d.kind == 0 && !d.ring && d.ndig >= 1 &&
+        if (pair_mode && psi_log_p(d.logR, MOA_C64) == 4 && d.lf_load && d.lf_store && d.kind == 0 && !d.ring &&
+            !mods.npeers && d.ndig >= 1 &&
             d.in_str[0] == 1 && d.out_str[0] == 1 && d.W >= 2 && d.logR >= min_lr && d.out_ksplit >= d.logR) {
             KArgs b = a;
             b.W = d.W / 2;
@@ -1894,6 +1905,10 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
         if (e != cudaErrorNotSupported) return e;
     }
     KFn<V> fn = tab[d.logR];
+    if (mods.npeers || d.ring) {  // the peer-store / ring paths live in the full instantiations
+        if constexpr (std::is_same<V, double2>::value) fn = kTabFull128[d.logR];
+        else fn = kTabFull64[d.logR];
+    }
     if (d.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
         if (e != cudaSuccess) return e;
