@@ -304,6 +304,42 @@ moa_status_t psi_3d_passes(int64_t n0, int64_t n1, int64_t n2, int64_t howmany, 
     // time, no scratch).  MOA_FFT_3D_ROT = 0 / 1 / 2 overrides (ablations).
     const char *rot_env = std::getenv("MOA_FFT_3D_ROT");
     const char rot = rot_env && *rot_env ? rot_env[0] : (dtype == MOA_C128 ? '2' : '0');
+    if (rot == '3' && howmany == 1 && n0 > 1 && n1 > 1 && n2 > 1) {
+        // z in place (contiguous both sides), then y and x with strided loads
+        // (one row apart: the L2 box prefetch applies) and plane-strided stores
+        // (merged into full lines in L2):
+        //   in [x][y][z] --z--> out [x][y][z] --y--> scratch [y][x][z] --x--> out [x][y][z]
+        moa_pass_desc_t d;
+        desc_init(d, log2_exact(n2));  // z: line (y, x), in place
+        add_digit(d, n1, n2, n2, 0);
+        add_digit(d, n0, plane, plane, 0);
+        d.in_kstr = d.out_kstr = 1;
+        d.src = 0;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n1));  // y: line (z, x) of [x][y][z], k_y -> scratch[k_y][x][z]
+        add_digit(d, n2, 1, 1, 0);
+        add_digit(d, n0, plane, n2, 0);
+        d.in_kstr = n2;
+        d.out_kstr = n0 * n2;
+        d.lf_load = d.lf_store = 1;
+        d.src = 1;
+        d.dst = 2;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        desc_init(d, log2_exact(n0));  // x: line (z, y) of [y][x][z], k_x -> out[k_x][y][z]
+        add_digit(d, n2, 1, 1, 0);
+        add_digit(d, n1, n0 * n2, n2, 0);
+        d.in_kstr = n2;
+        d.out_kstr = plane;
+        d.lf_load = d.lf_store = 1;
+        d.src = 2;
+        d.dst = 1;
+        psi_choose_tile(d, dtype);
+        out.push_back(d);
+        return MOA_OK;
+    }
     if (rot == '2' && howmany == 1 && n0 > 1 && n1 > 1 && n2 > 1) {
         // Rotating layouts, axis order z, x, y: every pass reads contiguous
         // lines and stores transposed so the next axis becomes contiguous (the

@@ -187,7 +187,7 @@ def test_planner_descriptors_compute_the_dft(n, batch, dtype):
             assert d["ext"][0] % d["W"] == 0
 
 
-@pytest.mark.parametrize("rot", ["0", "1", "2"])
+@pytest.mark.parametrize("rot", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_psi_3d_layouts(monkeypatch, rot, dtype):
     # in-place axis passes (0) and the two rotating-layout schedules (1: z,y,x;

@@ -204,7 +204,7 @@ def test_3d_fused_wide_planes(m, torch_cuda, monkeypatch, shape, dtype, rot):
 
 @pytest.mark.parametrize("shape", [(8, 8, 8), (4, 16, 32), (64, 32, 16), (2, 2, 2), (1, 8, 4), (128, 128, 128)])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
-@pytest.mark.parametrize("fuse,rot", [("", ""), ("1", "0"), ("", "0"), ("", "1"), ("", "2")])
+@pytest.mark.parametrize("fuse,rot", [("", ""), ("1", "0"), ("", "0"), ("", "1"), ("", "2"), ("", "3")])
 def test_3d(m, torch_cuda, monkeypatch, shape, dtype, fuse, rot):
     monkeypatch.setenv("MOA_FFT_FUSE", fuse)
     monkeypatch.setenv("MOA_FFT_3D_ROT", rot)
