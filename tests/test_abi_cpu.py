@@ -190,12 +190,15 @@ def test_planner_descriptors_compute_the_dft(n, batch, dtype):
 @pytest.mark.parametrize("rot", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_psi_3d_layouts(monkeypatch, rot, dtype):
-    # in-place axis passes (0) and the two rotating-layout schedules (1: z,y,x;
-    # 2: z,x,y -- every pass reads contiguous lines, stores transposed)
+    # in-place axis passes (0), the two rotating-layout schedules (1: z,y,x;
+    # 2: z,x,y -- every pass reads contiguous lines, stores transposed) and the
+    # mixed one (3: z in place, then strided loads / plane-strided stores)
     monkeypatch.setenv("MOA_FFT_3D_ROT", rot)
     for shape in [(8, 4, 16), (2, 32, 4), (16, 32, 64), (64, 8, 2)]:
         passes = m.moa_psi_describe_3d(*shape, dtype=dtype)
-        if rot != "0":
+        if rot == "3":
+            assert passes[0]["lf_load"] == 0 and passes[0]["lf_store"] == 0 and passes[-1]["dst"] == 1
+        elif rot != "0":
             assert all(d["lf_load"] == 0 for d in passes)          # contiguous loads only
             assert [d["dst"] for d in passes][-1] == 1
         x = synth.fill(int(np.prod(shape)), 7, synth.NORMAL)
