@@ -845,10 +845,10 @@ __device__ __forceinline__ void line_fft_pair(V (&pts)[16], V *sm, int LS, int l
 
 // A tile of the paired variant: load (16 points per thread), line DFT, lifted
 // weights, store -- the plain kernel's tile with the paired mappings.
-template <int LR, typename Sync = CtaSync, typename OnFree = NoFree>
-__device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2 *sm, int tid, const Sync &sync = Sync(),
+template <typename V, int LR, typename Sync = CtaSync, typename OnFree = NoFree>
+__device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, V *sm, int tid, const Sync &sync = Sync(),
                                           const OnFree &on_free = OnFree()) {
-    using V = double2;
+    using T = typename RealOf<V>::type;
     constexpr int R = 1 << LR, P = 16, TPL = R / P;
     // mappings: line-fast (lanes over the W lines; partner lane ^ W) or
     // point-fast (lanes over the points; partner lane ^ 1)
@@ -887,9 +887,9 @@ __device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2
         const double2 *__restrict__ lo = reinterpret_cast<const double2 *>(a.tw_lo);
         const int64_t lmask = (int64_t(1) << a.twh) - 1;
         const int64_t e0 = b_te + int64_t(lB) * a.tw_str[0] + a.tw_off;
-        auto tw = [&](int64_t e) {
+        auto tw = [&](int64_t e) {  // fp64 table product, rounded to V's precision
             e &= a.twmask;
-            return cmul(__ldg(hi + (e >> a.twh)), __ldg(lo + (e & lmask)));
+            return cvt_tw(cmul(__ldg(hi + (e >> a.twh)), __ldg(lo + (e & lmask))), V{});
         };
         const V w = tw(e0 * kb), s1 = tw(e0 * S1);
         V start[P / M1];
@@ -912,7 +912,7 @@ __device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2
         }
     }
     if (a.conj_out || a.scale != 1.0) {
-        const double sr = a.scale, si = a.conj_out ? -a.scale : a.scale;
+        const T sr = T(a.scale), si = a.conj_out ? -T(a.scale) : T(a.scale);
 #pragma unroll
         for (int m = 0; m < P; m++) pts[m] = mk<V>(pts[m].x * sr, pts[m].y * si);
     }
@@ -927,10 +927,10 @@ __device__ __forceinline__ void tile_pair(const KArgs &a, int64_t line0, double2
     }
 }
 
-template <int LR>
-__global__ void __launch_bounds__(512, 1) pass_kernel_pair(const KArgs a) {
+template <typename V, int LR>
+__global__ void __launch_bounds__(std::is_same<V, double2>::value ? 512 : 1024, 1) pass_kernel_pair(const KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    tile_pair<LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<double2 *>(smem_raw), threadIdx.x);
+    tile_pair<V, LR>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<V *>(smem_raw), threadIdx.x);
 }
 
 // (complex128 radix-32 kernels: at most 256 threads, so 255 registers -- a cap of
@@ -1886,11 +1886,11 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     }
     // MOA_FFT_PAIR=1: complex128 512- / 1024-point lines on thread pairs
     // (radix 32 with a warp-shuffle exchange, twice the threads per tile)
-    if constexpr (std::is_same<V, double2>::value) {
+    if constexpr (std::is_same<V, double2>::value || std::is_same<V, float2>::value) {
         const char *pe = std::getenv("MOA_FFT_PAIR");
         if (pe && pe[0] == '1' && (d.logR == 9 || d.logR == 10) && d.kind == 0 && !d.ring && !mods.npeers &&
-            2 * d.threads <= 512) {
-            auto fn = d.logR == 9 ? &pass_kernel_pair<9> : &pass_kernel_pair<10>;
+            2 * d.threads <= (std::is_same<V, double2>::value ? 512 : 1024)) {
+            auto fn = d.logR == 9 ? &pass_kernel_pair<V, 9> : &pass_kernel_pair<V, 10>;
             if (d.smem_bytes > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
                 if (e != cudaSuccess) return e;
