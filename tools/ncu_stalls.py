@@ -43,8 +43,25 @@ for name, lines in blocks:
         opc[op.split(".")[0]] += s
         for i in stall_cols:
             tot[h[i]] += int(r[i] or 0)
+    # dynamic instruction mix (warp-level instructions executed per opcode)
+    ie = next((i for i, c in enumerate(h) if c.strip() == "Instructions Executed"), None)
+    mix = Counter()
+    if ie is not None:
+        for r in rows[1:]:
+            if len(r) <= ie or not r[si].strip():
+                continue
+            op = r[si].strip().split()[0]
+            if op.startswith("@"):
+                op = r[si].strip().split()[1]
+            try:
+                mix[op.split(".")[0]] += int(float(r[ie] or 0))
+            except ValueError:
+                pass
     S = sum(tot.values()) or 1
     print(f"== {name[:90]}  samples {S}")
+    if mix:
+        M = sum(mix.values()) or 1
+        print(f"  executed (warp instructions {M}):", ", ".join(f"{k} {100 * v / M:.1f}%" for k, v in mix.most_common(14)))
     print("  stalls:", ", ".join(f"{k[6:]} {100 * v / S:.1f}%" for k, v in tot.most_common(8)))
     print("  by opcode:", ", ".join(f"{k} {100 * v / S:.1f}%" for k, v in opc.most_common(10)))
     for s, src in sorted(per, reverse=True)[:top]:
