@@ -269,7 +269,11 @@ typedef struct {
      * elements; ring = 1 marks the following pass B, which reads it back.  The
      * last line digit is the group; its stride on the ring side is replaced by
      * (group mod ring_slots) * ring_G.  ring_lag: groups between A and B in the
-     * tile order.  ring_discard: B drops the consumed lines from L2 (no write-back). */
+     * tile order.  ring_discard: B drops the consumed lines from L2 (no write-back).
+     * Cluster pair (the lifting at the thread-block-cluster level): ring = 3
+     * marks pass A, ring = 4 the following pass B; one launch, a cluster of
+     * ring_slots CTAs per group of ring_G elements, the intermediate in the
+     * cluster's distributed shared memory (never in HBM or the L2). */
     int32_t ring, ring_slots, ring_lag, ring_discard;
     int64_t ring_groups, ring_G;
 } moa_pass_desc_t;

@@ -526,7 +526,14 @@ moa_status_t moa_fft_exec(moa_fft_plan_t p, const void *in, void *out, void *str
             NvtxRange pass_range(nvtx_on() ? "pass " + std::to_string(i) + " R=" + std::to_string(1 << d.logR)
                                            : std::string());
             if (evs) cudaEventRecord(evs[step], s);
-            if (d.ring == 2) {  // fused pair: passes i and i+1 in one launch, intermediate in the L2 ring
+            if (d.ring == 3) {  // cluster pair: passes i and i+1 in one launch, intermediate in the clusters' smem
+                const moa_pass_desc_t &dB = p->passes[i + 1];
+                void *dst = dB.dst == 1 ? out : p->scratch;
+                e = launch_cluster(d, dB, p->dtype, src, dst, p->tabs[i], p->tabs[i + 1], s,
+                                   pass_mods(p->flags, i, np, p->n), pass_mods(p->flags, i + 1, np, p->n));
+                if (e != cudaSuccess) return cuda_fail(e, "cluster-pair kernel launch");
+                i++;
+            } else if (d.ring == 2) {  // fused pair: passes i and i+1 in one launch, intermediate in the L2 ring
                 const moa_pass_desc_t &dB = p->passes[i + 1];
                 void *dst = dB.dst == 1 ? out : p->scratch;
                 RingState &r = p->rings[i];
@@ -606,7 +613,7 @@ moa_status_t moa_fft_exec_host(moa_fft_plan_t p, const void *host_in, void *host
 
 static int local_launches(moa_fft_plan_t p) {
     int c = 0;
-    for (auto &d : p->passes) c += d.ring != 1;  // a fused pair is one launch
+    for (auto &d : p->passes) c += d.ring != 1 && d.ring != 4;  // a fused / cluster pair is one launch
     return c;
 }
 

@@ -242,6 +242,10 @@ struct alignas(64) KArgs {
     // CTAs ahead), so that tile's loads hit L2 instead of waiting on DRAM --
     // the paper's "pre-fetching becomes a deterministic cost"
     int64_t pf_dist, ntiles;
+    // cluster-level lifting (cluster_kernel): a group of 2^ds_lg elements is
+    // spread over the cluster's CTAs, 2^ds_lc elements in each one's shared memory
+    int32_t ds_lg, ds_lc;
+    int32_t ds_local;  // ablation (MOA_FFT_CLUSTER_LOCAL=1, wrong results): stores stay in the own CTA
 };
 
 __device__ __forceinline__ void line_offsets(const KArgs &a, int64_t line, int64_t &io, int64_t &oo, int64_t &te) {
@@ -300,6 +304,32 @@ __device__ __forceinline__ void st_pol(double2 *p, double2 v, uint64_t pol) {
 }
 __device__ __forceinline__ void st_pol(float2 *p, float2 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+
+// Distributed shared memory (the cluster level of the lifting): a store into
+// the shared memory of cluster CTA `rank` at the CTA-local address `la`, and
+// the cluster-wide barrier (release / acquire: the stores before it are
+// visible to every CTA of the cluster after it).
+__device__ __forceinline__ uint32_t cl_map(uint32_t la, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(la), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t ra, double2 v) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t ra, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(ra), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t, float4) {}  // (paired complex64 lines: not used)
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the same without the release fence: only orders this CTA's completed
+// shared-memory reads (values already in registers) before the other CTAs'
+// later stores into it (a write-after-read hazard, no data to publish)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
 // One Stockham step of radix Q = 2^LQ on a line of R = 2^LR points held as
@@ -437,7 +467,7 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a, i
 // compiled in; the plain pass kernel is built without them (their switched-off
 // branches cost the default path ~1 %, profiles/r3s_noopt.jsonl)
 template <typename V, int LR, typename Sync = CtaSync, typename OnFree = NoFree,
-          bool kEarlyTw = std::is_same<V, double2>::value, bool kFull = true>
+          bool kEarlyTw = std::is_same<V, double2>::value, bool kFull = true, bool kDs = false>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
                                              V (&pts)[1 << lp_of<V, LR>()], int64_t b_io, int64_t b_oo,
                                              int64_t b_te, int tid, const Sync &sync = Sync(),
@@ -579,6 +609,26 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
     }
 
     // ---- 4. store (128-bit; streaming to HBM, normal (L2-resident) to the ring)
+    if constexpr (kDs) {
+        // cluster level (cluster_kernel): the result goes straight into the
+        // shared memory of the cluster CTA whose pass-B tile reads it --
+        // position q of the group lives in CTA q >> ds_lc at offset q mod 2^ds_lc.
+        // First every CTA of the cluster must be done with its own shared memory
+        // (the block DFT's last exchange ended with a CTA barrier after its reads).
+        cluster_sync_relaxed();
+        const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        const int64_t gmask = (int64_t(1) << a.ds_lg) - 1, lmask = (int64_t(1) << a.ds_lc) - 1;
+        uint32_t own;
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(own));
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+            const int64_t q =
+                (oo + (a.ksplit >= LR ? int64_t(tB + m * TPL) * a.out_kstr : kaddr(a, tB + m * TPL))) & gmask;
+            const uint32_t rank = a.ds_local ? own : uint32_t(q >> a.ds_lc);
+            st_cluster(cl_map(base + uint32_t(q & lmask) * uint32_t(sizeof(V)), rank), pts[m]);
+        }
+        return;
+    }
     if (kFull && a.npeers) {  // fused all-to-all: send-layout offset q -> peer q / chunk (NVLink store)
         const uint64_t pol = l2_policy(false);
         const int64_t cmask = (int64_t(1) << a.log_chunk) - 1;
@@ -676,7 +726,7 @@ __device__ __forceinline__ void prefetch_tile_tensor(const KArgs &a, int64_t lin
 }
 
 // One tile with direct (register) loads -- the non-pipelined form.
-template <typename V, int LR, bool kFull = true>
+template <typename V, int LR, bool kFull = true, bool kDs = false>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
@@ -718,7 +768,7 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
             if constexpr (LPL == 2) pts[m].w = -pts[m].w;
         }
     }
-    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, kFull>(a, line0, sm, ring_off, pts, b_io, b_oo,
+    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, kFull, kDs>(a, line0, sm, ring_off, pts, b_io, b_oo,
                                                                               b_te, threadIdx.x);
 }
 
@@ -945,6 +995,41 @@ __global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double
                                   pass_min_blocks<V, LR>()) pass_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR, kFull>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
+}
+
+// ---------------------------------------------------------------------------
+// The cluster level of the lifting (MOA_FFT_CLUSTER): a two-pass lifting of
+// independent groups (cfg2: rows of 2^16 = 256 x 256 points) whose group fits
+// the shared memory of one thread-block cluster runs as ONE kernel, one HBM
+// round trip: a cluster of C CTAs owns one group; CTA c runs pass A's tile c
+// (loads from HBM, block DFTs, lifted weights) and stores its result straight
+// into the shared memory of the CTA that needs it (distributed shared memory,
+// the reshape-transpose of Eq. reshape3 P:2097-2114 done between SMs); after
+// the cluster barrier CTA c runs pass B's tile c from its own shared memory
+// and stores to HBM.  The paper's premise -- lift until a block fits one level
+// of the hierarchy -- with the cluster as the level between one
+// SM's shared memory and the L2.
+template <typename V, int LR>
+__global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512, 1)
+    cluster_kernel(const __grid_constant__ KArgs a, const __grid_constant__ KArgs b) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V *sm = reinterpret_cast<V *>(smem_raw);
+    constexpr int LP = lp_of<V, LR>();
+    constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
+    const int64_t tile = blockIdx.x;  // group tile / C, CTA rank tile % C (cluster dims (C, 1, 1))
+    tile_body<V, LR, false, true>(a, tile * a.W, sm, 0);
+    cluster_sync_all();  // every pass-A store of the cluster has landed
+    const TileMap mp = tile_map<TPL>(b, threadIdx.x);
+    int64_t b_io, b_oo, b_te;
+    line_offsets(b, tile * b.W, b_io, b_oo, b_te);
+    // pass B's tile reads exactly this CTA's slice (checked on the host)
+    const int64_t off = (b_io + int64_t(mp.lA) * b.in_str[0] + int64_t(mp.tA) * b.in_kstr) & ((int64_t(1) << b.ds_lc) - 1);
+    V pts[P];
+#pragma unroll
+    for (int m = 0; m < P; m++) pts[m] = sm[off + int64_t(m) * TPL * b.in_kstr];
+    __syncthreads();  // the block DFT's exchanges reuse the shared memory
+    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, false, false>(b, tile * b.W, sm, 0, pts, b_io,
+                                                                                     b_oo, b_te, threadIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1966,7 +2051,68 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(fn), dim3(unsigned(grid)),
                                        dim3(unsigned(dA.threads)), kargs, size_t(smem), stream);
 }
+
+template <typename V, int... Ls> constexpr auto make_cluster_table(std::integer_sequence<int, Ls...>) {
+    return std::array<void (*)(const KArgs, const KArgs), sizeof...(Ls)>{&cluster_kernel<V, 5 + Ls>...};
+}
+
+template <typename V>
+cudaError_t launch_cluster_t(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, const void *in, void *out,
+                             const DevTables &tA, const DevTables &tB, cudaStream_t stream, const PassMods &mA,
+                             const PassMods &mB) {
+    static const auto tab = make_cluster_table<V>(std::make_integer_sequence<int, 6>{});
+    if (dA.logR != dB.logR || dA.logR < 5 || dA.logR > 10 || dA.threads != dB.threads || dA.ring_slots < 1)
+        return cudaErrorInvalidValue;
+    const int esize = int(sizeof(V));
+    int64_t nA = 0, nB = 0;
+    KArgs a = fill_args(dA, in, nullptr, tA, &nA, mA, esize);
+    KArgs b = fill_args(dB, nullptr, out, tB, &nB, mB, esize);
+    const int C = dA.ring_slots;
+    const int lg = log2_exact(dA.ring_G), lc = lg - log2_exact(C);
+    a.ds_lg = b.ds_lg = lg;
+    a.ds_lc = b.ds_lc = lc;
+    auto fn = tab[dA.logR - 5];
+    int smem = dA.smem_bytes > dB.smem_bytes ? dA.smem_bytes : dB.smem_bytes;
+    if ((int64_t(1) << lc) * esize > smem) smem = int((int64_t(1) << lc) * esize);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && C > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    const int64_t tiles = nA / dA.W;  // groups x C
+    // pass A's loads: the plain kernel's L2 prefetch rule (launch_t)
+    const int64_t kload_b = dA.in_kstr * int64_t(esize);
+    double pf = (!dA.lf_load && dA.logR >= 9) ? 0.5 : (dA.lf_load && kload_b < (int64_t(1) << 20)) ? 0.5 : 0.0;
+    if (const char *pe = std::getenv(dA.lf_load ? "MOA_FFT_PF_LF" : "MOA_FFT_PF")) pf = std::atof(pe);
+    if (pf > 0 && (!dA.lf_load || set_lf_prefetch_map(a, dA, esize)))
+        set_prefetch(a, reinterpret_cast<const void *>(fn), dA.threads, smem, tiles, pf);
+    if (const char *le = std::getenv("MOA_FFT_CLUSTER_LOCAL")) a.ds_local = le[0] == '1';
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(tiles));
+    cfg.blockDim = dim3(unsigned(dA.threads));
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(C);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (std::getenv("MOA_FFT_VERBOSE")) {
+        int nc = -1;
+        cudaOccupancyMaxActiveClusters(&nc, reinterpret_cast<const void *>(fn), &cfg);
+        std::fprintf(stderr, "moa cluster pair: C=%d threads=%d smem=%d grid=%lld -> %d clusters resident\n", C,
+                     dA.threads, smem, (long long)tiles, nc);
+    }
+    return cudaLaunchKernelEx(&cfg, fn, a, b);
+}
 }  // namespace
+
+cudaError_t launch_cluster(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
+                           void *out, const DevTables &tA, const DevTables &tB, cudaStream_t stream,
+                           const PassMods &mA, const PassMods &mB) {
+    if (dtype == MOA_C128) return launch_cluster_t<double2>(dA, dB, in, out, tA, tB, stream, mA, mB);
+    return launch_cluster_t<float2>(dA, dB, in, out, tA, tB, stream, mA, mB);
+}
 
 cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void *in, void *out, const DevTables &tab,
                         cudaStream_t stream, const PassMods &mods) {

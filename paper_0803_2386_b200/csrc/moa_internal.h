@@ -87,6 +87,15 @@ cudaError_t launch_pass(const moa_pass_desc_t &d, moa_dtype_t dtype, const void 
 cudaError_t launch_pair(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
                         void *out, const RingState &rs, const DevTables &tA, const DevTables &tB, cudaStream_t stream,
                         const PassMods &mA = PassMods(), const PassMods &mB = PassMods());
+// The cluster level: passes A (ring == 3) and B (ring == 4) as one
+// thread-block-cluster kernel, the group in the cluster's shared memory
+// (ring_slots = CTAs per cluster, ring_G = elements per group).
+cudaError_t launch_cluster(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, moa_dtype_t dtype, const void *in,
+                           void *out, const DevTables &tA, const DevTables &tB, cudaStream_t stream,
+                           const PassMods &mA = PassMods(), const PassMods &mB = PassMods());
+// psi.cpp: a two-pass lifting of independent groups whose group fits one
+// cluster's shared memory becomes a cluster pair (returns 1 if made)
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype);
 // psi.cpp: fuse the passes of a one-GPU lifting into L2-staged pairs where the
 // group working set fits (marks ring fields; returns how many pairs were made)
 int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,

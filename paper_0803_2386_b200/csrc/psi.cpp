@@ -553,6 +553,43 @@ int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
     return fuse_two(passes, 0, dtype, 8, int64_t(64) << 20);
 }
 
+// The cluster level of the lifting (kernels.cu cluster_kernel): a two-pass
+// lifting of independent groups -- pass A's last line digit is the group, its
+// group stride G on the output side equals pass B's on the input side -- whose
+// group (G elements) fits the shared memory of one thread-block cluster of C
+// CTAs, C = pass A's tiles per group = pass B's tiles per group (<= 16).
+// Pass B's tile c must read exactly slice c of the group (contiguous rows of
+// R_B points), so its loads come from its own CTA's shared memory.
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
+    if (passes.size() != 2) return 0;
+    moa_pass_desc_t &A = passes[0], &B = passes[1];
+    const int64_t esize = dtype == MOA_C128 ? 16 : 8;
+    if (A.ring || B.ring || A.kind || B.kind || A.ndig != 2 || B.ndig != 2) return 0;
+    if (A.logR != B.logR || A.logR < 5 || A.logR > 10 || A.threads != B.threads) return 0;
+    if (A.dst != B.src || A.dst < 0) return 0;
+    const int64_t groups = A.ext[1], G = A.out_str[1], RB = int64_t(1) << B.logR;
+    if (B.ext[1] != groups || B.in_str[1] != G || (G & (G - 1))) return 0;
+    if (A.ext[0] % A.W || B.ext[0] % B.W) return 0;
+    const int64_t C = A.ext[0] / A.W;
+    if (C != B.ext[0] / B.W || C < 2 || C > 16 || (C & (C - 1))) return 0;
+    // pass B: contiguous rows of R_B points, rows adjacent -> tile c reads [c G/C, (c+1) G/C)
+    if (B.in_kstr != 1 || B.in_str[0] != RB || B.ext[0] * RB != G || B.lf_load) return 0;
+    if (A.out_ksplit < A.logR && A.out_kstr_hi == 0) return 0;
+    if ((G / C) * esize > 200 * 1024) return 0;
+    for (moa_pass_desc_t *d : {&A, &B}) {
+        d->ring_slots = int32_t(C);
+        d->ring_lag = 0;
+        d->ring_discard = 0;
+        d->ring_groups = groups;
+        d->ring_G = G;
+    }
+    A.ring = 3;
+    A.dst = -1;
+    B.ring = 4;
+    B.src = -1;
+    return 1;
+}
+
 // Four-pass lifting n = R0 R1 R2 R3 run as two L2-staged pairs, so a single
 // huge transform costs two HBM round trips (SURVEY §8(d.3)'s count for the
 // 2^14 x 2^14 / 2^15 x 2^15 six-step) with every per-CTA block <= 2^10 points.
@@ -680,7 +717,11 @@ moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::v
     }
     moa_status_t st = psi_lift_passes(n, batch, dtype, radices.data(), int(radices.size()), out);
     if (st) return st;
-    psi_fuse_pairs(out, radices, n, batch, dtype);
+    if (!psi_fuse_pairs(out, radices, n, batch, dtype)) {
+        // the cluster level (MOA_FFT_CLUSTER=1)
+        const char *ce = std::getenv("MOA_FFT_CLUSTER");
+        if (ce && ce[0] == '1') psi_cluster_pair(out, dtype);
+    }
     return MOA_OK;
 }
 
