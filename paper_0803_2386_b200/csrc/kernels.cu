@@ -180,6 +180,9 @@ template <int LQ, int H, typename V> __device__ __forceinline__ void dif_all(V *
         dif_all<LQ, H / 2>(v);
     }
 }
+#ifdef MOA_FFT_DIF_NET
+// (ablation build: the radix-2 decimation-in-frequency network with separate
+// complex rotations -- the round-1/2 default)
 template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
     constexpr int Q = 1 << LQ;
     if constexpr (Q > 1) {
@@ -191,6 +194,116 @@ template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
         for (int k = 0; k < Q; k++) v[k] = t[k];
     }
 }
+#else
+// Radix-2 decimation in time with FMA-shaped butterflies: the same radix-2
+// network (Fig. vanloan_fft's B_L stages), inputs taken in
+// bit-reversed register order (a compile-time renaming), spans 1, 2, ..., Q/2.
+// A butterfly (a, b) -> (a + w b, a - w b) with a nontrivial w = c + i s is
+// written w b = c (b + i tau b), tau = s / c (or w b = s (cot b + i b) when
+// |s| > |c|), so it costs 6 FMAs in complex128 (3 packed FFMA2 in complex64)
+// instead of a rotation (4) plus two complex adds (4): the 32-point DFT drops
+// from 456 to 388 FP64 instructions.  Twiddle constants w_32^E = cos(pi E/16)
+// - i sin(pi E/16) at compile time; the tangents of E = 4, 12 are exactly -/+1.
+constexpr double kCos16[9] = {1.0,
+                              0.98078528040323044913,
+                              0.92387953251128675613,
+                              0.83146961230254523708,
+                              0.70710678118654752440,
+                              0.55557023301960222474,
+                              0.38268343236508977173,
+                              0.19509032201612826785,
+                              0.0};
+template <int E> __host__ __device__ constexpr double w32_re() { return E <= 8 ? kCos16[E] : -kCos16[16 - E]; }
+template <int E> __host__ __device__ constexpr double w32_im() { return E <= 8 ? -kCos16[8 - E] : -kCos16[E - 8]; }
+// a <- a + w b, b <- a - w b with w b = f (u), u = b + i r b (tangent form:
+// f = c, r = s / c) or u = r b + i b (cotangent form: f = s, r = c / s)
+template <bool kTan> __device__ __forceinline__ void bfly_fma(double2 &a, double2 &b, double f, double r) {
+    double2 u;
+    if constexpr (kTan) u = make_double2(fma(-r, b.y, b.x), fma(r, b.x, b.y));
+    else u = make_double2(fma(r, b.x, -b.y), fma(r, b.y, b.x));
+    const double2 a0 = a;
+    a = make_double2(fma(f, u.x, a0.x), fma(f, u.y, a0.y));
+    b = make_double2(fma(-f, u.x, a0.x), fma(-f, u.y, a0.y));
+}
+#ifndef MOA_FFT_NO_F32X2
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long x, unsigned long long y, unsigned long long z) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(y), "l"(z));
+    return d;
+}
+template <bool kTan> __device__ __forceinline__ void bfly_fma(float2 &a, float2 &b, double f, double r) {
+    const float fr = float(r), ff = float(f);
+    // u = b + r (-b.y, b.x)  (tangent)  or  r b + (-b.y, b.x)  (cotangent)
+    const unsigned long long u = kTan ? ffma2(pk2(-b.y, b.x), pk2(fr, fr), pk2(b.x, b.y))
+                                      : ffma2(pk2(b.x, b.y), pk2(fr, fr), pk2(-b.y, b.x));
+    const unsigned long long a0 = pk2(a.x, a.y);
+    a = upk2(ffma2(pk2(ff, ff), u, a0));
+    b = upk2(ffma2(pk2(-ff, -ff), u, a0));
+}
+#else
+template <bool kTan> __device__ __forceinline__ void bfly_fma(float2 &a, float2 &b, double f, double r) {
+    const float fr = float(r), ff = float(f);
+    float2 u;
+    if constexpr (kTan) u = make_float2(fmaf(-fr, b.y, b.x), fmaf(fr, b.x, b.y));
+    else u = make_float2(fmaf(fr, b.x, -b.y), fmaf(fr, b.y, b.x));
+    const float2 a0 = a;
+    a = make_float2(fmaf(ff, u.x, a0.x), fmaf(ff, u.y, a0.y));
+    b = make_float2(fmaf(-ff, u.x, a0.x), fmaf(-ff, u.y, a0.y));
+}
+#endif
+template <bool kTan> __device__ __forceinline__ void bfly_fma(float4 &a, float4 &b, double f, double r) {
+    float2 al = lo2(a), ah = hi2(a), bl = lo2(b), bh = hi2(b);
+    bfly_fma<kTan>(al, bl, f, r);
+    bfly_fma<kTan>(ah, bh, f, r);
+    a = f4(al, ah);
+    b = f4(bl, bh);
+}
+// w_32^E b for the trivial E = 8 (-i): (b.y, -b.x)
+template <typename V> __device__ __forceinline__ V mul_mi(V b) {
+    if constexpr (std::is_same<V, float4>::value) return make_float4(b.y, -b.x, b.w, -b.z);
+    else return mk<V>(b.y, -b.x);
+}
+template <int E, typename V> __device__ __forceinline__ void dit_bfly_w(V &a, V &b) {
+    if constexpr (E == 0) {
+        const V a0 = a;
+        a = cadd(a0, b);
+        b = csub(a0, b);
+    } else if constexpr (E == 8) {
+        const V a0 = a, t = mul_mi(b);
+        a = cadd(a0, t);
+        b = csub(a0, t);
+    } else {
+        constexpr double c = w32_re<E>(), sn = w32_im<E>();
+        constexpr bool tan_form = (c < 0 ? -c : c) >= (sn < 0 ? -sn : sn);
+        if constexpr (tan_form) bfly_fma<true>(a, b, c, sn / c);
+        else bfly_fma<false>(a, b, sn, c / sn);
+    }
+}
+template <int H, int G, int I, typename V> __device__ __forceinline__ void dit_bfly(V *v) {
+    dit_bfly_w<I *(16 / H)>(v[G + I], v[G + I + H]);  // w_{2H}^I = w_32^{16 I / H}
+}
+template <int H, typename V, int... Is> __device__ __forceinline__ void dit_span(V *v, std::integer_sequence<int, Is...>) {
+    (dit_bfly<H, (Is / H) * 2 * H, Is % H>(v), ...);
+}
+template <int LQ, int H, typename V> __device__ __forceinline__ void dit_all(V *v) {
+    if constexpr (H < (1 << LQ)) {
+        dit_span<H>(v, std::make_integer_sequence<int, (1 << LQ) / 2>{});
+        dit_all<LQ, 2 * H>(v);
+    }
+}
+template <int LQ, typename V> __device__ __forceinline__ void dft_reg(V *v) {
+    constexpr int Q = 1 << LQ;
+    static_assert(Q <= 32, "register DFTs of at most 32 points");
+    if constexpr (Q > 1) {
+        V t[Q];
+#pragma unroll
+        for (int k = 0; k < Q; k++) t[k] = v[brev<LQ>(k)];
+        dit_all<LQ, 1>(t);
+#pragma unroll
+        for (int k = 0; k < Q; k++) v[k] = t[k];
+    }
+}
+#endif
 
 // Shared-memory position of element i of a line: one pad element per 16, so
 // the radix-16 stride-16 writes of step 0 and the unit-stride reads are
@@ -2000,6 +2113,28 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     }
     if (pf > 0 && !d.ring && (!d.lf_load || set_lf_prefetch_map(a, d, int(sizeof(typename ElemOf<V>::type)))))
         set_prefetch(a, reinterpret_cast<const void *>(fn), d.threads, d.smem_bytes, tiles, pf);
+    // ablation (MOA_FFT_CLAUNCH=k): launch a line-fast pass whose loads are
+    // >= 1 MiB apart as clusters of k CTAs, so the k adjacent tiles (whose
+    // 128-byte runs share DRAM pages) start together on one GPC
+    static const int claunch = [] {
+        const char *ce = std::getenv("MOA_FFT_CLAUNCH");
+        return ce ? std::atoi(ce) : 0;
+    }();
+    if (claunch > 1 && d.lf_load && kload_b >= (int64_t(1) << 20) && tiles % claunch == 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(tiles));
+        cfg.blockDim = dim3(unsigned(d.threads));
+        cfg.dynamicSmemBytes = size_t(d.smem_bytes);
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = unsigned(claunch);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fn, a);
+    }
     fn<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
     return cudaGetLastError();
 }
