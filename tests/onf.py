@@ -23,7 +23,7 @@ def enumerate_pass(d):
         io += dig * si
         oo += dig * so
         te += dig * st
-    if d.get("ring", 0):
+    if d.get("ring", 0) in (1, 2):
         # the slowest line bits are the group; on the ring side it addresses slot (g mod slots)
         grp = line // (nlines // d["ring_groups"])
         slot = (grp & (d["ring_slots"] - 1)) * d["ring_G"]
@@ -82,6 +82,15 @@ def run_plan(passes, x):
             for g in range(d["ring_groups"]):          # lines of a group are contiguous in ONF order
                 run_pass(d, bufs[d["src"]], ring, slice(g * la, (g + 1) * la), ea)
                 run_pass(B, ring, bufs[B["dst"]], slice(g * lb, (g + 1) * lb), eb)
+            i += 2
+            continue
+        if d.get("ring", 0) == 3:
+            # cluster pair: A's stores land in the cluster's shared memory at their
+            # group positions (the descriptors keep the plain layout), B reads them
+            B = passes[i + 1]
+            tmp = np.full(x.size, np.nan + 0j)
+            run_pass(d, bufs[d["src"]], tmp)
+            run_pass(B, tmp, bufs[B["dst"]])
             i += 2
             continue
         run_pass(d, bufs[d["src"]], bufs[d["dst"]])

@@ -317,6 +317,33 @@ def test_fused_pair_descriptors_compute_the_dft(monkeypatch):
     assert [d["ring"] for d in p2] == [2, 1]
 
 
+@pytest.mark.parametrize("n,batch,dtype,C", [(1 << 16, 3, "c128", 16), (1 << 14, 2, "c128", 8), (1 << 16, 2, "c64", 16)])
+def test_cluster_pair_descriptors(monkeypatch, n, batch, dtype, C):
+    """The cluster level (MOA_FFT_CLUSTER=1, kernels.cu cluster_kernel): every
+    group's pass-A stores stay inside the group (they go to the cluster's
+    shared memory, slice q >> log2(G/C)), pass-B tile c of a group reads exactly
+    slice c (its own CTA's shared memory), and the pair computes the DFT."""
+    monkeypatch.setenv("MOA_FFT_CLUSTER", "1")
+    A, B = m.moa_psi_describe(n, batch, dtype)
+    assert (A["ring"], B["ring"]) == (3, 4)
+    G, CC = A["ring_G"], A["ring_slots"]
+    assert G == n and CC == C and A["ring_groups"] == batch
+    _, sa, _ = enumerate_pass(A)
+    la = np.arange(sa.shape[0]) // (sa.shape[0] // batch)
+    assert (sa // G == la[:, None]).all()
+    assert np.array_equal(np.sort(sa.ravel()), np.arange(n * batch))
+    lb, _, _ = enumerate_pass(B)
+    tile = np.arange(lb.shape[0]) // B["W"]
+    assert ((lb % G) // (G // CC) == (tile % CC)[:, None]).all()
+    assert (lb // G == (tile // CC)[:, None]).all()
+    x = synth.fill(n * batch, 17, synth.UNIFORM)
+    got = run_plan([A, B], x)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+    monkeypatch.delenv("MOA_FFT_CLUSTER")
+    assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == [0, 0]  # opt-in
+
+
 # ---------------------------------------------------------------- Ch.6 density-matrix gate (host side)
 def test_qgate_transpose_vector_and_view_offsets_bit_exact_vs_oracle():
     from oracle import qgate
