@@ -1100,12 +1100,16 @@ __global__ void __launch_bounds__(std::is_same<V, double2>::value ? 512 : 1024, 
 // 168 for three CTAs per SM spills and measured slower, profiles/r1_s7_radix32.txt;
 // complex64 ones fit 512 threads at 128 registers: 16-line tiles, 128-byte runs;
 // complex64 lines of <= 256 points keep two 512-thread CTAs per SM)
-template <typename V, int LR> constexpr int pass_min_blocks() {  // 2 CTAs of 512 threads: <= 64 registers
-    return (std::is_same<V, float2>::value && lp_of<V, LR>() <= 4) ? 2 : 1;
+// (complex64 kernels of <= 16 points per thread: <= 64 registers, i.e. two
+// 512-thread CTAs or one 1024-thread CTA per SM -- the 1024-thread tiles of the
+// >= 2^11-point transposing passes, psi_choose_tile)
+template <typename V, int LR> constexpr int pass_max_threads() {
+    return (lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256
+           : (std::is_same<V, float2>::value && lp_of<V, LR>() <= 4) ? 1024
+                                                                      : 512;
 }
 template <typename V, int LR, bool kFull = false>
-__global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512,
-                                  pass_min_blocks<V, LR>()) pass_kernel(const __grid_constant__ KArgs a) {
+__global__ void __launch_bounds__(pass_max_threads<V, LR>(), 1) pass_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR, kFull>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
 }

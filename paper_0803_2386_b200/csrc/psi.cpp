@@ -94,13 +94,28 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // complex64 radix-32 passes loading contiguous lines and storing transposed:
     // 16-line tiles too (128-byte store runs at one 512-thread CTA per SM;
     // measured cfg4's 1024^3 last pass 3.54 -> 3.20 ms, profiles/r3c_c64.jsonl)
-    const bool c64_wide = esize == 8 && logP == 5 && !d.lf_load && d.lf_store;
+    // (and line-coalesced loads of 1024-point complex64 lines at any stride:
+    // 16 lines, 128-byte runs -- measured cfg4's middle pass 3.42 -> 3.40 ms,
+    // the 3-D complex64 y-pass 3.29 -> 3.10-3.15 ms, profiles/r5n_cap.jsonl)
+    const bool c64_wide = esize == 8 && logP == 5 && (d.lf_load || d.lf_store);
+    // complex64 lines of >= 2^11 points (16 points per thread) storing
+    // transposed: 8 lines per tile (64-byte store runs, one 1024-thread CTA per
+    // SM at 64 registers) instead of the 4 that two CTAs per SM allow
+    // (MOA_FFT_C64_WIDE2=0 restores 4)
+    static const bool wide2_on = [] {
+        const char *e = std::getenv("MOA_FFT_C64_WIDE2");
+        return !(e && e[0] == '0');
+    }();
+    // (only where the stores are >= 1 MiB apart: the 2^30 plans' 2048-point last
+    // pass 6.0 -> 4.1 ms; 4 KiB apart (batched 2^20) 0.245 -> 0.258 ms, r5m / r5o)
+    const bool c64_wide2 = wide2_on && esize == 8 && logP == 4 && logR >= 11 && d.lf_store &&
+                           d.out_kstr * esize >= (int64_t(1) << 20);
     const int64_t smem_cap = cap_env ? std::atoll(cap_env)
-                                     : ((d.lf_load && kload >= (int64_t(1) << 20)) || c64_wide ? 200000 : 100 * 1024);
+                                     : ((d.lf_load && kload >= (int64_t(1) << 20)) || c64_wide || c64_wide2 ? 200000 : 100 * 1024);
     // ablation knobs: lines per tile for line-coalesced / point-contiguous passes
     const char *wenv = std::getenv(lf ? "MOA_FFT_W_LF" : "MOA_FFT_W_PF");
     if (wenv && std::atoi(wenv) > 0) W = std::atoi(wenv);
-    const int64_t max_thr = (logP == 5 && esize == 16) ? 256 : 512;  // complex128 radix-32 kernels keep 255 registers
+    const int64_t max_thr = (logP == 5 && esize == 16) ? 256 : c64_wide2 ? 1024 : 512;  // complex128 radix-32 kernels keep 255 registers
     while (W > 1 && (W * R * esize > smem_cap || W * TPL > max_thr || ext0 % W)) W >>= 1;
     if (W < 1) W = 1;
     set_tile(d, dtype, W);
