@@ -589,7 +589,6 @@ int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
     if (C != B.ext[0] / B.W || C < 2 || C > 16 || (C & (C - 1))) return 0;
     // pass B: contiguous rows of R_B points, rows adjacent -> tile c reads [c G/C, (c+1) G/C)
     if (B.in_kstr != 1 || B.in_str[0] != RB || B.ext[0] * RB != G || B.lf_load) return 0;
-    if (A.out_ksplit < A.logR && A.out_kstr_hi == 0) return 0;
     if ((G / C) * esize > 200 * 1024) return 0;
     for (moa_pass_desc_t *d : {&A, &B}) {
         d->ring_slots = int32_t(C);
@@ -713,6 +712,28 @@ static moa_status_t lift4_fused(int64_t n, int64_t batch, moa_dtype_t dtype, con
     return MOA_OK;
 }
 
+// Ablation (MOA_FFT_W_PASS="i:W,j:W"): pass i of a 1-D plan gets W lines per
+// tile (when W divides the line digit and the tile fits 1024 threads and 227 KiB).
+static void apply_w_pass_env(std::vector<moa_pass_desc_t> &v, moa_dtype_t dtype) {
+    const char *e = std::getenv("MOA_FFT_W_PASS");
+    if (!e) return;
+    const int esize = dtype == MOA_C128 ? 16 : 8;
+    for (const char *q = e; *q;) {
+        char *end = nullptr;
+        const long i = std::strtol(q, &end, 10);
+        if (!end || *end != ':') return;
+        const long W = std::strtol(end + 1, &end, 10);
+        if (i >= 0 && size_t(i) < v.size() && W >= 1 && (W & (W - 1)) == 0) {
+            moa_pass_desc_t &d = v[size_t(i)];
+            const int64_t R = int64_t(1) << d.logR, TPL = R >> psi_log_p(d.logR, dtype);
+            const int64_t ext0 = d.ndig ? d.ext[0] : 1;
+            if (ext0 % W == 0 && W * TPL <= 1024 && W * (R + R / 16 + 32) * esize <= 227 * 1024) set_tile(d, dtype, W);
+        }
+        if (*end != ',') return;
+        q = end + 1;
+    }
+}
+
 moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::vector<int64_t> &radices, bool planned,
                        std::vector<moa_pass_desc_t> &out) {
     // the four-factor lifting as two L2-staged pairs is opt-in (MOA_FFT_LIFT4=1):
@@ -732,6 +753,7 @@ moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::v
     }
     moa_status_t st = psi_lift_passes(n, batch, dtype, radices.data(), int(radices.size()), out);
     if (st) return st;
+    apply_w_pass_env(out, dtype);
     if (!psi_fuse_pairs(out, radices, n, batch, dtype)) {
         // the cluster level (MOA_FFT_CLUSTER=1)
         const char *ce = std::getenv("MOA_FFT_CLUSTER");
