@@ -273,7 +273,8 @@ typedef struct {
      * Cluster pair (the lifting at the thread-block-cluster level): ring = 3
      * marks pass A, ring = 4 the following pass B; one launch, a cluster of
      * ring_slots CTAs per group of ring_G elements, the intermediate in the
-     * cluster's distributed shared memory (never in HBM or the L2). */
+     * cluster's distributed shared memory (never in HBM or the L2); ring_lag
+     * holds the buffer id the intermediate had in the plain two-pass form. */
     int32_t ring, ring_slots, ring_lag, ring_discard;
     int64_t ring_groups, ring_G;
 } moa_pass_desc_t;

@@ -333,6 +333,7 @@ void hypercube_passes(int64_t n, int64_t batch, std::vector<moa_pass_desc_t> &ou
 // transpose; the natural descriptor is kept for moa_fft_output_index.
 void make_lifted_order(moa_fft_plan_s *p) {
     if (p->passes.size() < 2) return;  // a single pass is already in natural order
+    psi_uncluster(p->passes);          // the last pass is rewritten below
     moa_pass_desc_t &d = p->passes.back();
     if (d.ring) return;                // fused L2 pairs keep natural order
     p->natural_last = d;

@@ -95,7 +95,8 @@ cudaError_t launch_cluster(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB,
                            const PassMods &mA = PassMods(), const PassMods &mB = PassMods());
 // psi.cpp: a two-pass lifting of independent groups whose group fits one
 // cluster's shared memory becomes a cluster pair (returns 1 if made)
-int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype);
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas);
+void psi_uncluster(std::vector<moa_pass_desc_t> &passes);
 // psi.cpp: fuse the passes of a one-GPU lifting into L2-staged pairs where the
 // group working set fits (marks ring fields; returns how many pairs were made)
 int psi_fuse_pairs(std::vector<moa_pass_desc_t> &passes, const std::vector<int64_t> &radices, int64_t n, int64_t batch,

@@ -575,7 +575,7 @@ int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
 // CTAs, C = pass A's tiles per group = pass B's tiles per group (<= 16).
 // Pass B's tile c must read exactly slice c of the group (contiguous rows of
 // R_B points), so its loads come from its own CTA's shared memory.
-int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas) {
     if (passes.size() != 2) return 0;
     moa_pass_desc_t &A = passes[0], &B = passes[1];
     const int64_t esize = dtype == MOA_C128 ? 16 : 8;
@@ -586,13 +586,13 @@ int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
     if (B.ext[1] != groups || B.in_str[1] != G || (G & (G - 1))) return 0;
     if (A.ext[0] % A.W || B.ext[0] % B.W) return 0;
     const int64_t C = A.ext[0] / A.W;
-    if (C != B.ext[0] / B.W || C < 2 || C > 16 || (C & (C - 1))) return 0;
+    if (C != B.ext[0] / B.W || C < 2 || C > max_ctas || C > 16 || (C & (C - 1))) return 0;
     // pass B: contiguous rows of R_B points, rows adjacent -> tile c reads [c G/C, (c+1) G/C)
     if (B.in_kstr != 1 || B.in_str[0] != RB || B.ext[0] * RB != G || B.lf_load) return 0;
     if ((G / C) * esize > 200 * 1024) return 0;
     for (moa_pass_desc_t *d : {&A, &B}) {
         d->ring_slots = int32_t(C);
-        d->ring_lag = 0;
+        d->ring_lag = A.dst;  // (the intermediate's buffer id, for psi_uncluster)
         d->ring_discard = 0;
         d->ring_groups = groups;
         d->ring_G = G;
@@ -602,6 +602,21 @@ int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
     B.ring = 4;
     B.src = -1;
     return 1;
+}
+
+// Back to the two plain passes (the plan variants that rewrite the last pass,
+// e.g. the lifted output order, take the plain form).
+void psi_uncluster(std::vector<moa_pass_desc_t> &passes) {
+    for (size_t i = 0; i + 1 < passes.size(); i++) {
+        moa_pass_desc_t &A = passes[i], &B = passes[i + 1];
+        if (A.ring != 3 || B.ring != 4) continue;
+        A.dst = B.src = A.ring_lag;
+        for (moa_pass_desc_t *d : {&A, &B}) {
+            d->ring = 0;
+            d->ring_slots = d->ring_lag = d->ring_discard = 0;
+            d->ring_groups = d->ring_G = 0;
+        }
+    }
 }
 
 // Four-pass lifting n = R0 R1 R2 R3 run as two L2-staged pairs, so a single
@@ -755,9 +770,14 @@ moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::v
     if (st) return st;
     apply_w_pass_env(out, dtype);
     if (!psi_fuse_pairs(out, radices, n, batch, dtype)) {
-        // the cluster level (MOA_FFT_CLUSTER=1)
+        // the cluster level: by default where a group spreads over <= 8 CTAs
+        // (measured: 2^14-point complex128 rows, 8-CTA clusters of 128 threads,
+        // 0.643 -> 0.593 ms for 4096 rows; 16-CTA clusters -- cfg2's 2^16-point
+        // rows -- are slower than the two passes, 0.98 vs 0.64 ms, so only with
+        // MOA_FFT_CLUSTER=1; MOA_FFT_CLUSTER=0: never)
         const char *ce = std::getenv("MOA_FFT_CLUSTER");
-        if (ce && ce[0] == '1') psi_cluster_pair(out, dtype);
+        const int64_t max_c = !ce ? 8 : ce[0] == '1' ? 16 : 0;
+        if (max_c) psi_cluster_pair(out, dtype, max_c);
     }
     return MOA_OK;
 }

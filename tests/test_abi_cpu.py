@@ -341,8 +341,10 @@ def test_cluster_pair_descriptors(monkeypatch, n, batch, dtype, C):
     got = run_plan([A, B], x)
     ref = oracle.fft_radix2_rows(x, n)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
-    monkeypatch.delenv("MOA_FFT_CLUSTER")
-    assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == [0, 0]  # opt-in
+    monkeypatch.delenv("MOA_FFT_CLUSTER")  # default: clusters of <= 8 CTAs only
+    assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == ([3, 4] if C <= 8 else [0, 0])
+    monkeypatch.setenv("MOA_FFT_CLUSTER", "0")
+    assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == [0, 0]
 
 
 # ---------------------------------------------------------------- Ch.6 density-matrix gate (host side)

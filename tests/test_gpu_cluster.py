@@ -99,6 +99,23 @@ def test_cluster_pair_cfg2_shape(m, torch_cuda):
     assert np.array_equal(xt.cpu().numpy().view(np.uint8), y.view(np.uint8))
 
 
+def test_cluster_pair_default_for_small_clusters(m, torch_cuda):
+    """By default the cluster level is used where a row spreads over <= 8 CTAs
+    (2^14-point complex128 rows), not for cfg2's 16-CTA rows."""
+    old = os.environ.pop("MOA_FFT_CLUSTER", None)
+    try:
+        p14 = m.FFTPlan(1 << 14, 5, "c128")
+        p16 = m.FFTPlan(1 << 16, 5, "c128")
+        assert rings(p14) == [3, 4] and p14.describe()[0]["ring_slots"] == 8 and p14.launches == 1
+        assert rings(p16) == [0, 0] and p16.launches == 2
+        x = synth.fill((1 << 14) * 5, 79, synth.UNIFORM)
+        y = p14.exec(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_l2(y, oracle.fft_radix2_rows(x, 1 << 14)) <= 1e-11
+    finally:
+        if old is not None:
+            os.environ["MOA_FFT_CLUSTER"] = old
+
+
 @pytest.mark.parametrize("normalize", [False, True])
 def test_cluster_pair_inverse(m, torch_cuda, normalize):
     torch = torch_cuda

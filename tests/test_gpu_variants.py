@@ -75,8 +75,11 @@ def test_inverse_3d(m, torch_cuda, shape):
 
 
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
-@pytest.mark.parametrize("n,batch", [(1 << 10, 2), (1 << 13, 3), (1 << 16, 2), (1 << 20, 1), (1 << 24, 1)])
+@pytest.mark.parametrize("n,batch", [(1 << 10, 2), (1 << 13, 3), (1 << 14, 3), (1 << 16, 2), (1 << 20, 1),
+                                     (1 << 24, 1)])
 def test_lifted_order_1d(m, torch_cuda, dtype, n, batch):
+    # (2^14 complex128 rows are a cluster pair in natural order; lifted order
+    # takes the plain two-pass form)
     x = synth.fill(n * batch, 81, synth.UNIFORM, dtype)
     plan = m.FFTPlan(n, batch, dtype, lifted_order=True)
     pos = plan.output_index()
