@@ -434,7 +434,6 @@ __device__ __forceinline__ void st_cluster(uint32_t ra, double2 v) {
 __device__ __forceinline__ void st_cluster(uint32_t ra, float2 v) {
     asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(ra), "f"(v.x), "f"(v.y) : "memory");
 }
-__device__ __forceinline__ void st_cluster(uint32_t, float4) {}  // (paired complex64 lines: not used)
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
