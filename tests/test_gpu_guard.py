@@ -41,6 +41,9 @@ def guarded(torch, data, dtype):
     dict(n=1 << 14, batch=2, kw={"lifted_order": True}), dict(n=1 << 12, batch=2, kw={"unblocked": True}),
     dict(n=1 << 13, batch=2, kw={"inverse": True, "normalize": True}),
     dict(shape=(16, 32, 64)), dict(shape=(32, 16, 8), dtype="c64"), dict(shape=(8, 8, 8), env={"MOA_FFT_3D_ROT": "0"}),
+    # the cluster pair: 8-CTA (default) and 16-CTA (forced) clusters
+    dict(n=1 << 14, batch=3), dict(n=1 << 16, batch=3, env={"MOA_FFT_CLUSTER": "1"}),
+    dict(n=1 << 16, batch=2, dtype="c64", env={"MOA_FFT_CLUSTER": "1"}),
 ])
 def test_no_out_of_bounds_writes(m, torch_cuda, monkeypatch, case):
     torch = torch_cuda

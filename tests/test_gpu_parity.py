@@ -348,3 +348,24 @@ def test_cfg5_full(m, torch_cuda):
     err = rel_l2_chunked(y, ref.reshape(-1))
     print(f"cfg5 whole-vector rel-L2 {err:.3e}")
     assert err <= 1e-11
+
+
+@pytest.mark.parametrize("radices,wpass", [([256, 512, 2048], "2:4"), ([1024, 1024, 256], "0:8,1:8")])
+def test_c64_wide_tiles_bit_exact(m, torch_cuda, monkeypatch, radices, wpass):
+    """Round 2 session 2's complex64 tile rules (16-line tiles for 1024-point
+    line-coalesced passes; 8-line 1024-thread tiles for >= 2^11-point passes
+    storing >= 1 MiB apart) change only which lines share a CTA, so the result
+    is bit-identical to the narrower tiles (MOA_FFT_W_PASS), and on sampled
+    bins within the tolerance of the oracle's definition."""
+    n = 1 << 28
+    x = synth.fill(n, 23, synth.UNIFORM, "c64")
+    wide = m.FFTPlan(n, 1, "c64", radices=radices)
+    monkeypatch.setenv("MOA_FFT_W_PASS", wpass)
+    narrow = m.FFTPlan(n, 1, "c64", radices=radices)
+    ww, wn = [d["W"] for d in wide.describe()], [d["W"] for d in narrow.describe()]
+    assert ww != wn and max(d["threads"] for d in wide.describe()) >= 512
+    y = gpu_run(torch_cuda, wide, x)
+    y2 = gpu_run(torch_cuda, narrow, x)
+    assert np.array_equal(y.view(np.uint8), y2.view(np.uint8))
+    bins = np.array([0, 1, 2047, 1 << 17, (1 << 20) + 3, n // 2, n - 1], dtype=np.int64)
+    _sampled_bins_check(x, y, n, bins, 2e-5)
