@@ -383,12 +383,17 @@ __device__ __forceinline__ int64_t kaddr(const KArgs &a, int k) {
 }
 
 // 128-bit / 64-bit global accesses with an L2 eviction-policy operand, so the
-// streaming HBM side (evict_first) and the L2 ring (evict_last) share one code
-// path; loads bypass L1 (.cg): ring slots are rewritten by other SMs.
+// streaming HBM side (evict_normal) and the L2 ring (evict_last) share one
+// code path; loads bypass L1 (.cg): ring slots are rewritten by other SMs.
+// (The streaming side was evict_first until round 2, session 2: evict_normal
+// measured cfg4 10.93 -> 10.78 ms, cfg3 -0.4 ... -1.3 %, cfg2 / cfg5 within
+// noise -- the strided first passes' 128-byte runs share DRAM fetches with
+// the neighbouring tile's, which evict_first dropped early;
+// profiles/r5w_policy.jsonl, r5x2_policy.jsonl.)
 __device__ __forceinline__ uint64_t l2_policy(bool keep) {
     uint64_t p;
     if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ double2 ld_pol(const double2 *p, uint64_t pol) {
