@@ -65,9 +65,13 @@ typedef struct moa_fft_plan_s *moa_fft_plan_t; /* opaque, library-owned */
  *            in = x[g n/p, (g+1) n/p) and receives out = X[g n/p, (g+1) n/p).
  * The lifting n = R_0 R_1 ... is chosen by the planner; the environment
  * variable MOA_FFT_LIFT="r0,r1,..." overrides it (the paper's run-time blocking
- * size c; for ablations).  Allocates device scratch (one buffer of
- * the local data size, only when the lifting has more than one pass) and the
- * twiddle tables on the current device.
+ * size c; for ablations).  A two-pass lifting of rows that spread
+ * over <= 8 CTAs (e.g. 2^14-point complex128 rows) runs as one cluster pair
+ * (ring = 3 / 4 below: the intermediate in distributed shared memory, one
+ * launch; MOA_FFT_CLUSTER=0 disables it, =1 allows 16-CTA clusters too).
+ * Allocates device scratch (one buffer of the local data size, only when the
+ * lifting has more than one launch that needs it) and the twiddle tables on
+ * the current device.
  */
 moa_status_t moa_fft_plan(moa_fft_plan_t *plan, int64_t n, int64_t batch, moa_dtype_t dtype, int ngpu);
 
