@@ -94,10 +94,16 @@ void psi_choose_tile(moa_pass_desc_t &d, moa_dtype_t dtype) {
     // complex64 radix-32 passes loading contiguous lines and storing transposed:
     // 16-line tiles too (128-byte store runs at one 512-thread CTA per SM;
     // measured cfg4's 1024^3 last pass 3.54 -> 3.20 ms, profiles/r3c_c64.jsonl)
-    // (and line-coalesced loads of 1024-point complex64 lines at any stride:
-    // 16 lines, 128-byte runs -- measured cfg4's middle pass 3.42 -> 3.40 ms,
-    // the 3-D complex64 y-pass 3.29 -> 3.10-3.15 ms, profiles/r5n_cap.jsonl)
-    const bool c64_wide = esize == 8 && logP == 5 && (d.lf_load || d.lf_store);
+    // (and line-coalesced loads of 1024-point complex64 lines without lifted
+    // weights at any stride: 16 lines, 128-byte runs -- measured the 3-D
+    // complex64 y-pass 3.29 -> 3.10-3.15 ms, profiles/r5n_cap.jsonl; with the
+    // weights' table lookups two 8-line CTAs per SM hide latency better: cfg4's
+    // middle pass 3.40 (16 lines) vs 3.17 ms (8 lines), profiles/r6d_lfw.jsonl)
+    static const bool lfw_on = [] {  // MOA_FFT_C64_LFW=0: 8 lines on the line-coalesced loads
+        const char *e = std::getenv("MOA_FFT_C64_LFW");
+        return !(e && e[0] == '0');
+    }();
+    const bool c64_wide = esize == 8 && logP == 5 && ((lfw_on && d.lf_load && d.twN <= 1) || (!d.lf_load && d.lf_store));
     // complex64 lines of >= 2^11 points (16 points per thread) storing
     // transposed: 8 lines per tile (64-byte store runs, one 1024-thread CTA per
     // SM at 64 registers) instead of the 4 that two CTAs per SM allow

@@ -96,11 +96,11 @@ def test_bench_config_tiles():
     assert [(1 << d["logR"], d["W"], d["threads"]) for d in d2] == [(256, 16, 256), (256, 16, 256)]
     # cfg4: three 1024-point complex64 passes (radix 32 x 32 on the FP32x2 pipe);
     # 16-line tiles (128-byte runs) where the loads are >= 1 MiB apart and where
-    # contiguous lines are stored transposed, and (round 2, session 2) for the
-    # 8 KiB-strided middle pass too (profiles/r5n_cap.jsonl)
+    # contiguous lines are stored transposed; 8 lines for the 8 KiB-strided middle
+    # pass, whose lifted weights favour two CTAs per SM (profiles/r6d_lfw.jsonl)
     d4 = m.moa_psi_describe(1 << 30, 1, "c64")
     assert [1 << d["logR"] for d in d4] == [1024, 1024, 1024]
-    assert [d["W"] for d in d4] == [16, 16, 16] and [d["threads"] for d in d4] == [512, 512, 512]
+    assert [d["W"] for d in d4] == [16, 8, 16] and [d["threads"] for d in d4] == [512, 256, 512]
     # the four-factor lifting it replaced: the 32 MiB-strided first pass takes 32 lines
     d4b = m.moa_psi_describe(1 << 30, 1, "c64", [256, 128, 128, 256])
     assert d4b[0]["W"] == 32 and d4b[0]["threads"] == 512 and d4b[1]["W"] == 16
