@@ -1129,16 +1129,22 @@ __global__ void __launch_bounds__(pass_max_threads<V, LR>(), 1) pass_kernel(cons
 // the cluster barrier CTA c runs pass B's tile c from its own shared memory
 // and stores to HBM.  The paper's premise -- lift until a block fits one level
 // of the hierarchy -- with the cluster as the level between one
-// SM's shared memory and the L2.
-template <typename V, int LR>
-__global__ void __launch_bounds__((lp_of<V, LR>() == 5 && std::is_same<V, double2>::value) ? 256 : 512, 1)
+// SM's shared memory and the L2.  The two passes may have different radices
+// (R_A = 2^LRA, R_B = 2^LRB) with the same number of points per thread, so one
+// CTA size serves both (psi_cluster_pair picks the tile widths).
+template <typename V, int LRA, int LRB>
+__global__ void __launch_bounds__(((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5) && std::is_same<V, double2>::value)
+                                      ? 256
+                                      : 512,
+                                  1)
     cluster_kernel(const __grid_constant__ KArgs a, const __grid_constant__ KArgs b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V *sm = reinterpret_cast<V *>(smem_raw);
+    constexpr int LR = LRB;
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
     const int64_t tile = blockIdx.x;  // group tile / C, CTA rank tile % C (cluster dims (C, 1, 1))
-    tile_body<V, LR, false, true>(a, tile * a.W, sm, 0);
+    tile_body<V, LRA, false, true>(a, tile * a.W, sm, 0);
     cluster_sync_all();  // every pass-A store of the cluster has landed
     const TileMap mp = tile_map<TPL>(b, threadIdx.x);
     int64_t b_io, b_oo, b_te;
@@ -2195,16 +2201,17 @@ cudaError_t launch_pair_t(const std::array<PFn<V>, 36> &tab, const moa_pass_desc
                                        dim3(unsigned(dA.threads)), kargs, size_t(smem), stream);
 }
 
-template <typename V, int... Ls> constexpr auto make_cluster_table(std::integer_sequence<int, Ls...>) {
-    return std::array<void (*)(const KArgs, const KArgs), sizeof...(Ls)>{&cluster_kernel<V, 5 + Ls>...};
+// (R_A, R_B) in 2^5 .. 2^9 (25 instantiations per dtype)
+template <typename V, int... Is> constexpr auto make_cluster_table(std::integer_sequence<int, Is...>) {
+    return std::array<void (*)(const KArgs, const KArgs), sizeof...(Is)>{&cluster_kernel<V, 5 + Is / 5, 5 + Is % 5>...};
 }
 
 template <typename V>
 cudaError_t launch_cluster_t(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB, const void *in, void *out,
                              const DevTables &tA, const DevTables &tB, cudaStream_t stream, const PassMods &mA,
                              const PassMods &mB) {
-    static const auto tab = make_cluster_table<V>(std::make_integer_sequence<int, 6>{});
-    if (dA.logR != dB.logR || dA.logR < 5 || dA.logR > 10 || dA.threads != dB.threads || dA.ring_slots < 1)
+    static const auto tab = make_cluster_table<V>(std::make_integer_sequence<int, 25>{});
+    if (dA.logR < 5 || dA.logR > 9 || dB.logR < 5 || dB.logR > 9 || dA.threads != dB.threads || dA.ring_slots < 1)
         return cudaErrorInvalidValue;
     const int esize = int(sizeof(V));
     int64_t nA = 0, nB = 0;
@@ -2214,7 +2221,7 @@ cudaError_t launch_cluster_t(const moa_pass_desc_t &dA, const moa_pass_desc_t &d
     const int lg = log2_exact(dA.ring_G), lc = lg - log2_exact(C);
     a.ds_lg = b.ds_lg = lg;
     a.ds_lc = b.ds_lc = lc;
-    auto fn = tab[dA.logR - 5];
+    auto fn = tab[(dA.logR - 5) * 5 + (dB.logR - 5)];
     int smem = dA.smem_bytes > dB.smem_bytes ? dA.smem_bytes : dB.smem_bytes;
     if ((int64_t(1) << lc) * esize > smem) smem = int((int64_t(1) << lc) * esize);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -95,7 +95,7 @@ cudaError_t launch_cluster(const moa_pass_desc_t &dA, const moa_pass_desc_t &dB,
                            const PassMods &mA = PassMods(), const PassMods &mB = PassMods());
 // psi.cpp: a two-pass lifting of independent groups whose group fits one
 // cluster's shared memory becomes a cluster pair (returns 1 if made)
-int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas);
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas, int64_t max_threads);
 void psi_uncluster(std::vector<moa_pass_desc_t> &passes);
 // psi.cpp: fuse the passes of a one-GPU lifting into L2-staged pairs where the
 // group working set fits (marks ring fields; returns how many pairs were made)

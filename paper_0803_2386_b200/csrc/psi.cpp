@@ -581,33 +581,48 @@ int psi_fuse_3d(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype) {
 // CTAs, C = pass A's tiles per group = pass B's tiles per group (<= 16).
 // Pass B's tile c must read exactly slice c of the group (contiguous rows of
 // R_B points), so its loads come from its own CTA's shared memory.
-int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas) {
+int psi_cluster_pair(std::vector<moa_pass_desc_t> &passes, moa_dtype_t dtype, int64_t max_ctas, int64_t max_threads) {
     if (passes.size() != 2) return 0;
     moa_pass_desc_t &A = passes[0], &B = passes[1];
     const int64_t esize = dtype == MOA_C128 ? 16 : 8;
     if (A.ring || B.ring || A.kind || B.kind || A.ndig != 2 || B.ndig != 2) return 0;
-    if (A.logR != B.logR || A.logR < 5 || A.logR > 10 || A.threads != B.threads) return 0;
+    if (A.logR < 5 || A.logR > 9 || B.logR < 5 || B.logR > 9) return 0;
+    const int lp = psi_log_p(A.logR, dtype);
+    if (psi_log_p(B.logR, dtype) != lp) return 0;  // one CTA size for both passes
     if (A.dst != B.src || A.dst < 0) return 0;
-    const int64_t groups = A.ext[1], G = A.out_str[1], RB = int64_t(1) << B.logR;
+    const int64_t groups = A.ext[1], G = A.out_str[1], RA = int64_t(1) << A.logR, RB = int64_t(1) << B.logR;
     if (B.ext[1] != groups || B.in_str[1] != G || (G & (G - 1))) return 0;
-    if (A.ext[0] % A.W || B.ext[0] % B.W) return 0;
-    const int64_t C = A.ext[0] / A.W;
-    if (C != B.ext[0] / B.W || C < 2 || C > max_ctas || C > 16 || (C & (C - 1))) return 0;
     // pass B: contiguous rows of R_B points, rows adjacent -> tile c reads [c G/C, (c+1) G/C)
     if (B.in_kstr != 1 || B.in_str[0] != RB || B.ext[0] * RB != G || B.lf_load) return 0;
-    if ((G / C) * esize > 200 * 1024) return 0;
-    for (moa_pass_desc_t *d : {&A, &B}) {
-        d->ring_slots = int32_t(C);
-        d->ring_lag = A.dst;  // (the intermediate's buffer id, for psi_uncluster)
-        d->ring_discard = 0;
-        d->ring_groups = groups;
-        d->ring_G = G;
+    // C CTAs per group: pass A's tile c = lines [c W_A, (c+1) W_A), pass B's the
+    // same with W_B; both tiles have n / (C P) threads.  The largest C (smallest
+    // CTAs, most clusters resident) with a legal tile on both sides
+    const int64_t cap_thr = (esize == 16 && lp == 5) ? 256 : 512;
+    const int64_t smem_cap = 100 * 1024;
+    for (int64_t C = max_ctas < 16 ? max_ctas : 16; C >= 2; C >>= 1) {
+        if (A.ext[0] % C || B.ext[0] % C) continue;
+        const int64_t WA = A.ext[0] / C, WB = B.ext[0] / C;
+        const int64_t thr = WA * (RA >> lp);
+        if (thr != WB * (RB >> lp) || thr > cap_thr || thr > max_threads || thr < 64) continue;
+        if (WA * (RA + RA / 16 + 32) * esize > smem_cap || WB * (RB + RB / 16 + 32) * esize > smem_cap ||
+            (G / C) * esize > smem_cap)
+            continue;
+        if (WA != A.W) set_tile(A, dtype, WA);
+        if (WB != B.W) set_tile(B, dtype, WB);
+        for (moa_pass_desc_t *d : {&A, &B}) {
+            d->ring_slots = int32_t(C);
+            d->ring_lag = A.dst;  // (the intermediate's buffer id, for psi_uncluster)
+            d->ring_discard = 0;
+            d->ring_groups = groups;
+            d->ring_G = G;
+        }
+        A.ring = 3;
+        A.dst = -1;
+        B.ring = 4;
+        B.src = -1;
+        return 1;
     }
-    A.ring = 3;
-    A.dst = -1;
-    B.ring = 4;
-    B.src = -1;
-    return 1;
+    return 0;
 }
 
 // Back to the two plain passes (the plan variants that rewrite the last pass,
@@ -776,14 +791,22 @@ moa_status_t psi_build(int64_t n, int64_t batch, moa_dtype_t dtype, const std::v
     if (st) return st;
     apply_w_pass_env(out, dtype);
     if (!psi_fuse_pairs(out, radices, n, batch, dtype)) {
-        // the cluster level: by default where a group spreads over <= 8 CTAs
-        // (measured: 2^14-point complex128 rows, 8-CTA clusters of 128 threads,
-        // 0.643 -> 0.593 ms for 4096 rows; 16-CTA clusters -- cfg2's 2^16-point
-        // rows -- are slower than the two passes, 0.98 vs 0.64 ms, so only with
-        // MOA_FFT_CLUSTER=1; MOA_FFT_CLUSTER=0: never)
+        // the cluster level, by default where it measured faster than the two
+        // passes (profiles/r6i_cluster2.jsonl, 512 MiB of rows): complex128 rows
+        // on 8-CTA clusters of <= 128 threads (2^13: 0.88x, 2^14: 0.93x; 2^15
+        // at 256 threads 1.25x; complex64 1.17-1.48x), and any <= 8-CTA,
+        // <= 256-thread cluster pair when the whole batch is <= 32 MiB (one
+        // launch instead of two: 0.74-0.91x).  16-CTA clusters -- cfg2's
+        // 2^16-point rows -- are slower (0.98 vs 0.64 ms): only with
+        // MOA_FFT_CLUSTER=1 (any C <= 16); MOA_FFT_CLUSTER=0: never
         const char *ce = std::getenv("MOA_FFT_CLUSTER");
-        const int64_t max_c = !ce ? 8 : ce[0] == '1' ? 16 : 0;
-        if (max_c) psi_cluster_pair(out, dtype, max_c);
+        if (!ce) {
+            const int64_t bytes = n * batch * (dtype == MOA_C128 ? 16 : 8);
+            const int64_t mt = bytes <= (int64_t(32) << 20) ? 256 : dtype == MOA_C128 ? 128 : 0;
+            if (mt) psi_cluster_pair(out, dtype, 8, mt);
+        } else if (ce[0] == '1') {
+            psi_cluster_pair(out, dtype, 16, 512);
+        }
     }
     return MOA_OK;
 }

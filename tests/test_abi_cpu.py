@@ -318,8 +318,10 @@ def test_fused_pair_descriptors_compute_the_dft(monkeypatch):
     assert [d["ring"] for d in p2] == [2, 1]
 
 
-@pytest.mark.parametrize("n,batch,dtype,C", [(1 << 16, 3, "c128", 16), (1 << 14, 2, "c128", 8), (1 << 16, 2, "c64", 16)])
-def test_cluster_pair_descriptors(monkeypatch, n, batch, dtype, C):
+@pytest.mark.parametrize("n,batch,dtype,C,C_default", [
+    (1 << 16, 3, "c128", 16, 0), (1 << 14, 2, "c128", 16, 8), (1 << 16, 2, "c64", 16, 0),
+    (1 << 13, 3, "c128", 8, 8), (1 << 15, 2, "c128", 16, 8), (1 << 14, 3, "c64", 16, 8), (1 << 13, 2, "c64", 8, 8)])
+def test_cluster_pair_descriptors(monkeypatch, n, batch, dtype, C, C_default):
     """The cluster level (MOA_FFT_CLUSTER=1, kernels.cu cluster_kernel): every
     group's pass-A stores stay inside the group (they go to the cluster's
     shared memory, slice q >> log2(G/C)), pass-B tile c of a group reads exactly
@@ -341,8 +343,11 @@ def test_cluster_pair_descriptors(monkeypatch, n, batch, dtype, C):
     got = run_plan([A, B], x)
     ref = oracle.fft_radix2_rows(x, n)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
-    monkeypatch.delenv("MOA_FFT_CLUSTER")  # default: clusters of <= 8 CTAs only
-    assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == ([3, 4] if C <= 8 else [0, 0])
+    monkeypatch.delenv("MOA_FFT_CLUSTER")  # default: clusters of <= 8 CTAs of <= 256 threads
+    dd = m.moa_psi_describe(n, batch, dtype)
+    assert [d["ring"] for d in dd] == ([3, 4] if C_default else [0, 0])
+    if C_default:
+        assert dd[0]["ring_slots"] == C_default and dd[0]["threads"] == dd[1]["threads"] <= 256
     monkeypatch.setenv("MOA_FFT_CLUSTER", "0")
     assert [d["ring"] for d in m.moa_psi_describe(n, batch, dtype)] == [0, 0]
 
