@@ -304,7 +304,11 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
     def run_exec():
         m.moa_fft_exec(ph, xp, yp, sh)
 
-    m.moa_fft_prof_begin(plan.h, steps)
+    # per-launch events (moa_fft_prof_*) ride inside the timed loop, except for
+    # the latency-bound small configs, where their records would be part of the
+    # step: those take the per-launch times from a separate loop afterwards
+    if not small:
+        m.moa_fft_prof_begin(plan.h, steps)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)] if small else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(ctx["local"]) as clk:
@@ -324,6 +328,12 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
             end.record(stream)
             barrier()
             total_ms = start.elapsed_time(end)
+    if small:
+        m.moa_fft_prof_begin(plan.h, steps)
+        for i in range(steps):
+            flush.fill_(i & 0xFF)
+            run_exec()
+        barrier()
     step_ms_list, nexec = m.moa_fft_prof_end(plan.h)
     ms = total_ms / steps
     if dist:
@@ -472,7 +482,31 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
             a1.record(stream)
             a1.synchronize()
             fl.append(a0.elapsed_time(a1) * 1e3)
-        latency = {"plain_launch_us": plain_us, "plain_launch_l2_flushed_us": round(sorted(fl)[len(fl) // 2], 2),
+        # device-side time of one call: a sleep kernel ahead of the events keeps
+        # the GPU busy while the host enqueues, so the host's submission time
+        # stays outside the event pair (the flushed figure above gets the same
+        # effect from its fill kernel)
+        dv = []
+        for i in range(200):
+            torch.cuda._sleep(20000)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            run_exec()
+            a1.record(stream)
+            a1.synchronize()
+            dv.append(a0.elapsed_time(a1) * 1e3)
+        de = []
+        for i in range(200):
+            torch.cuda._sleep(20000)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            torch.cuda._sleep(0)
+            a1.record(stream)
+            a1.synchronize()
+            de.append(a0.elapsed_time(a1) * 1e3)
+        latency = {"device_us_warm": round(sorted(dv)[len(dv) // 2], 2),
+                   "device_empty_kernel_us": round(sorted(de)[len(de) // 2], 2),
+                   "plain_launch_us": plain_us, "plain_launch_l2_flushed_us": round(sorted(fl)[len(fl) // 2], 2),
                    "python_wrapper_us": wrapper_us, "cuda_graph_us": graph_us, "l2": "warm unless stated",
                    "reps": 1000, "how": "CUDA events around one moa_fft_exec C-ABI call (ctypes), median"}
 

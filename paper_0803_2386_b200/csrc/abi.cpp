@@ -179,6 +179,27 @@ moa_status_t build_tables(moa_fft_plan_s *p) {
             if (st) return st;
             byR[d.logR] = t.twR;
         }
+        if (p->passes.size() == 1 && d.kind == 0 && d.twN <= 1 && d.logR >= 6 && d.logR <= 12) {
+            // the small-transform kernel's table (kernels.cu small_fft_kernel):
+            // radix-4 step s >= 1 with NS = 4^s stores w_{4 NS}^{k q} (k < NS,
+            // 1 <= q < 4) at entry (NS - 4) + (q - 1) NS + k; an odd log2 R adds
+            // the final radix-2 step's w_R^j (j < R/2) at (R/2 - 4) + j
+            const int64_t R = int64_t(1) << d.logR;
+            std::vector<long double> v(2 * (R - 4), 0.0L);
+            for (int64_t NS = 4; 4 * NS <= R; NS *= 4)
+                for (int64_t q = 1; q < 4; q++)
+                    for (int64_t k = 0; k < NS; k++) {
+                        const int64_t idx = (NS - 4) + (q - 1) * NS + k;
+                        omega_ld(k * q, 4 * NS, v[2 * idx], v[2 * idx + 1]);
+                    }
+            if (d.logR & 1)
+                for (int64_t j = 0; j < R / 2; j++) {
+                    const int64_t idx = (R / 2 - 4) + j;
+                    omega_ld(j, R, v[2 * idx], v[2 * idx + 1]);
+                }
+            moa_status_t st = upload_table(p, v, &t.twS);
+            if (st) return st;
+        }
         if (d.twN > 1) {
             auto jt = byN.find(d.twN);
             if (jt != byN.end()) {

@@ -332,7 +332,7 @@ struct alignas(64) KArgs {
     int32_t lext[kMaxDigits];  // log2 extents
     int32_t ndig;
     int64_t in_kstr, out_kstr;
-    const void *twR, *tw_hi, *tw_lo;
+    const void *twR, *tw_hi, *tw_lo, *twS;
     int64_t twmask;  // twN - 1 (0: no twiddle)
     int64_t tw_off;  // exponent base offset (processor-level lifting)
     int32_t twh;     // split bit of the two-level table
@@ -1543,29 +1543,21 @@ __global__ void __launch_bounds__(((lp_of<V, LRA>() == 5 || lp_of<V, LRB>() == 5
 // transform).  One CTA per line, R/4 threads: radix-4 Stockham steps (the
 // self-sorting form of the radix-2 network, Fig. vanloan_fft, two
 // stages per step) ping-ponging between two shared-memory buffers, one barrier
-// per step; the table w_R^e (e < 3R/4) is computed in the prologue with
-// sincospi while the line's loads are in flight, so no dependent table load
-// waits on DRAM; the first step runs straight from the loaded registers and the
-// last one stores to global memory in natural order.
-template <typename V> __device__ __forceinline__ V tw_exact(int e, int R);
-template <> __device__ __forceinline__ double2 tw_exact<double2>(int e, int R) {
-    double s, c;
-    sincospi(2.0 * double(e) / double(R), &s, &c);
-    return make_double2(c, -s);
-}
-template <> __device__ __forceinline__ float2 tw_exact<float2>(int e, int R) {
-    // complex64: the angle in double, rounded once (~1 ulp of float)
-    double s, c;
-    sincospi(2.0 * double(e) / double(R), &s, &c);
-    return make_float2(float(c), float(-s));
-}
+// per step.  The step twiddles come from the plan's table (abi.cpp
+// build_tables, twS: step s >= 1 with NS = 4^s holds w_{4 NS}^{k q} at
+// (NS - 4) + (q - 1) NS + k, so a step's reads are unit-stride across the
+// threads; an odd log2 R appends w_R^j at R/2 - 4 + j), copied to shared
+// memory in the prologue with loads issued together with the line's, so the
+// two DRAM latencies overlap and no twiddle is computed.  The first step runs
+// straight from the loaded registers and the last one stores to global memory
+// in natural order.
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }  // one pad element per 16
 
 template <typename V, int LR>
 __global__ void __launch_bounds__((1 << LR) / 4) small_fft_kernel(const KArgs a) {
     constexpr int R = 1 << LR, T = R / 4, NT4 = LR / 2;  // radix-4 steps; odd LR adds a radix-2 step
     constexpr bool R2 = (LR & 1) != 0;
-    constexpr int TW = 3 * R / 4;
+    constexpr int TW = R - 4, TWT = (TW + T - 1) / T;   // table entries, per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V *buf0 = reinterpret_cast<V *>(smem_raw);
     V *buf1 = buf0 + spad(R);
@@ -1575,10 +1567,16 @@ __global__ void __launch_bounds__((1 << LR) / 4) small_fft_kernel(const KArgs a)
     int64_t io, oo, te;
     line_offsets(a, int64_t(blockIdx.x), io, oo, te);
     const E *in = reinterpret_cast<const E *>(a.in) + io;
-    V v[4];
+    const E *tws = reinterpret_cast<const E *>(a.twS);
+    V v[4], wt[TWT];
 #pragma unroll
     for (int q = 0; q < 4; q++) v[q] = in[t + q * T];
-    for (int e = t; e < TW; e += T) tw[e] = tw_exact<V>(e, R);
+#pragma unroll
+    for (int i = 0; i < TWT; i++)
+        if (t + i * T < TW) wt[i] = __ldg(tws + t + i * T);
+#pragma unroll
+    for (int i = 0; i < TWT; i++)
+        if (t + i * T < TW) tw[t + i * T] = wt[i];
     if (a.conj_in) {
 #pragma unroll
         for (int q = 0; q < 4; q++) v[q].y = -v[q].y;
@@ -1591,10 +1589,10 @@ __global__ void __launch_bounds__((1 << LR) / 4) small_fft_kernel(const KArgs a)
         if (s > 0) {
 #pragma unroll
             for (int q = 0; q < 4; q++) v[q] = src[spad(t + q * T)];
-            // twiddles w_{4 NS}^{k q} = w_R^{k q R / (4 NS)}
-            const int k = t & (NS - 1), st = R / (4 * NS);
+            // twiddles w_{4 NS}^{k q}
+            const int k = t & (NS - 1);
 #pragma unroll
-            for (int q = 1; q < 4; q++) v[q] = cmul(v[q], tw[k * q * st]);
+            for (int q = 1; q < 4; q++) v[q] = cmul(v[q], tw[(NS - 4) + (q - 1) * NS + k]);
         }
         // radix-4 DFT (w_4 = -i)
         const V a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
@@ -1623,7 +1621,7 @@ __global__ void __launch_bounds__((1 << LR) / 4) small_fft_kernel(const KArgs a)
         for (int g = 0; g < 2; g++) {
             const int j = t + g * T;
             V x0 = src[spad(j)], x1 = src[spad(j + R / 2)];
-            x1 = cmul(x1, tw[j]);  // w_R^{j}
+            x1 = cmul(x1, tw[(R / 2 - 4) + j]);  // w_R^{j}
             w[g] = cadd(x0, x1);
             w[2 + g] = csub(x0, x1);
         }
@@ -1803,6 +1801,7 @@ KArgs fill_args(const moa_pass_desc_t &d, const void *in, void *out, const DevTa
     a.twR = tb.twR;
     a.tw_hi = tb.tw_hi;
     a.tw_lo = tb.tw_lo;
+    a.twS = tb.twS;
     a.twmask = d.twN > 1 ? d.twN - 1 : 0;
     const int lN = log2_exact(d.twN);
     a.twh = (lN + 1) / 2;
@@ -2068,7 +2067,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
     }
     // one-pass plans with few lines (latency, cfg1): the small-transform kernel
     // (MOA_FFT_SMALL=0 disables it)
-    if (d.kind == 0 && !d.ring && !mods.npeers && d.twN <= 1 && d.logR >= 6 && d.logR <= 12 && !d.lf_load &&
+    if (d.kind == 0 && tb.twS && !d.ring && !mods.npeers && d.twN <= 1 && d.logR >= 6 && d.logR <= 12 && !d.lf_load &&
         !d.lf_store && d.in_kstr == 1 && d.out_kstr == 1 && d.out_ksplit >= d.logR && nlines <= 64) {
         const char *se = std::getenv("MOA_FFT_SMALL");
         if (!(se && se[0] == '0')) {
@@ -2077,7 +2076,7 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                                                         &small_fft_kernel<V, 10>, &small_fft_kernel<V, 11>,
                                                         &small_fft_kernel<V, 12>};
             const int R = 1 << d.logR;
-            const size_t smem = (2 * size_t(R + (R >> 4)) + size_t(3 * R / 4)) * sizeof(V);
+            const size_t smem = (2 * size_t(R + (R >> 4)) + size_t(R - 4)) * sizeof(V);
             KFn<V> fn = small[d.logR - 6];
             static std::mutex mu;
             static std::map<std::pair<int, const void *>, size_t> attr;  // opt-in smem set once per (device, kernel)

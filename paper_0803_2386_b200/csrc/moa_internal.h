@@ -50,6 +50,8 @@ struct DevTables {
     const void *twR = nullptr;   // this pass's in-line Stockham step twiddles (step-major, R - 1 entries)
     const void *tw_hi = nullptr; // w_N^{eh 2^h}
     const void *tw_lo = nullptr; // w_N^{el}
+    const void *twS = nullptr;   // one-pass 2^6..2^12-point plans: the small-transform kernel's
+                                 // radix-4 step twiddles (R - 4 entries, kernels.cu small_fft_kernel)
     unsigned long long *ctr = nullptr;  // this pass's tile counter (warp-specialised kernel), or null
 };
 // Device state of the L2 ring of a fused pass pair (owned by the plan).
