@@ -370,7 +370,14 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
                 launches_l.append(("pair", f"pair_kernel<{vt},{desc[i]['logR']},{desc[i + 1]['logR']}>"))
                 i += 2
             else:
-                launches_l.append(("pass", f"pass_kernel<{vt},{desc[i]['logR']}>"))
+                dd = desc[i]
+                # the TMA-store form (kernels.cu launch_t: complex128 512- / 1024-point
+                # passes, contiguous loads, transposed stores >= 8 MiB apart)
+                st_env = os.environ.get("MOA_FFT_TMA_ST")
+                tma_st = (vt == "double2" and dd["logR"] in (9, 10) and not dd["lf_load"] and dd["lf_store"]
+                          and dd.get("kind", 0) == 0 and not dd["ring"]
+                          and (st_env == "1" if st_env is not None else dd["out_kstr"] * 16 >= 8 << 20))
+                launches_l.append(("pass", f"pass_kernel{'_st' if tma_st else ''}<{vt},{dd['logR']}>"))
                 i += 1
     per_step = [s / max(nexec, 1) for s in step_ms_list]
     if len(launches_l) != len(per_step):

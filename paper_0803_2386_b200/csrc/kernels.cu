@@ -325,7 +325,11 @@ struct alignas(64) KArgs {
     // of W lines x 256 points -- one prefetch instruction per box instead of one
     // per 128-byte run
     CUtensorMap pf_tmap;
+    // TMA store of a line-fast store side (MOA_FFT_TMA_ST, pass_kernel_st):
+    // tensor map over the output, boxes of W lines x 256 points
+    CUtensorMap st_tmap;
     int32_t pf_rank, pf_nbox, pf_box_pts, pf_ext0;
+    int32_t st_rank, st_nbox, st_box_pts;
     const void *in;
     void *out;
     int64_t in_str[kMaxDigits], out_str[kMaxDigits], tw_str[kMaxDigits];
@@ -584,7 +588,7 @@ template <int TPL> __device__ __forceinline__ TileMap tile_map(const KArgs &a, i
 // compiled in; the plain pass kernel is built without them (their switched-off
 // branches cost the default path ~1 %, profiles/r3s_noopt.jsonl)
 template <typename V, int LR, typename Sync = CtaSync, typename OnFree = NoFree,
-          bool kEarlyTw = std::is_same<V, double2>::value, bool kFull = true, bool kDs = false>
+          bool kEarlyTw = std::is_same<V, double2>::value, bool kFull = true, bool kDs = false, bool kSt = false>
 __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *sm, int64_t ring_off,
                                              V (&pts)[1 << lp_of<V, LR>()], int64_t b_io, int64_t b_oo,
                                              int64_t b_te, int tid, const Sync &sync = Sync(),
@@ -746,6 +750,58 @@ __device__ __forceinline__ void tile_compute(const KArgs &a, int64_t line0, V *s
         }
         return;
     }
+    if constexpr (kSt) {
+        // TMA store (MOA_FFT_TMA_ST): the tile is staged in shared memory in the
+        // output's order -- point k of line l at k W + l, i.e. W-element runs,
+        // consecutive lanes at consecutive addresses -- and leaves as
+        // R / 256 tensor-map boxes (W lines x 256 points) through the TMA
+        // (cp.async.bulk.tensor ... global.shared::cta), so the SM issues no
+        // per-point stores: the transposed side's runs go out as bulk writes.
+        sync();  // every thread's last exchange reads are done
+#pragma unroll
+        for (int m = 0; m < P; m++) sm[(tB + m * TPL) * a.W + lB] = pts[m];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        sync();
+        if (tid < a.st_nbox) {
+            int32_t c[5] = {0, 0, 0, 0, 0};
+            int64_t rest = line0;
+            c[0] = int32_t(2 * (rest % a.pf_ext0));
+            rest /= a.pf_ext0;
+            for (int i = 1; i < a.ndig && i + 1 < 5; i++) {
+                c[i + 1] = int32_t(rest & ((int64_t(1) << a.lext[i]) - 1));
+                rest >>= a.lext[i];
+            }
+            c[1] = tid * a.st_box_pts;
+            const uint64_t t = reinterpret_cast<uint64_t>(&a.st_tmap);
+            const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(sm + int64_t(tid) * a.st_box_pts * a.W));
+            switch (a.st_rank) {
+                case 2:
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(t),
+                                 "r"(c[0]), "r"(c[1]), "r"(src)
+                                 : "memory");
+                    break;
+                case 3:
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(t),
+                                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(src)
+                                 : "memory");
+                    break;
+                case 4:
+                    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(t),
+                                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(src)
+                                 : "memory");
+                    break;
+                default:
+                    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(t),
+                                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src)
+                                 : "memory");
+                    break;
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            // the CTA's shared memory must outlive the TMA's reads of it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        return;
+    }
     if (kFull && a.npeers) {  // fused all-to-all: send-layout offset q -> peer q / chunk (NVLink store)
         const uint64_t pol = l2_policy(false);
         const int64_t cmask = (int64_t(1) << a.log_chunk) - 1;
@@ -843,7 +899,7 @@ __device__ __forceinline__ void prefetch_tile_tensor(const KArgs &a, int64_t lin
 }
 
 // One tile with direct (register) loads -- the non-pipelined form.
-template <typename V, int LR, bool kFull = true, bool kDs = false>
+template <typename V, int LR, bool kFull = true, bool kDs = false, bool kSt = false>
 __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, int64_t ring_off) {
     constexpr int LP = lp_of<V, LR>();
     constexpr int P = 1 << LP, R = 1 << LR, TPL = R / P;
@@ -885,7 +941,7 @@ __device__ __forceinline__ void tile_body(const KArgs &a, int64_t line0, V *sm, 
             if constexpr (LPL == 2) pts[m].w = -pts[m].w;
         }
     }
-    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, kFull, kDs>(a, line0, sm, ring_off, pts, b_io, b_oo,
+    tile_compute<V, LR, CtaSync, NoFree, std::is_same<V, double2>::value, kFull, kDs, kSt>(a, line0, sm, ring_off, pts, b_io, b_oo,
                                                                               b_te, threadIdx.x);
 }
 
@@ -1116,6 +1172,12 @@ template <typename V, int LR, bool kFull = false>
 __global__ void __launch_bounds__(pass_max_threads<V, LR>(), 1) pass_kernel(const __grid_constant__ KArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     tile_body<V, LR, kFull>(a, int64_t(blockIdx.x) * a.W * lines_per_lane<V>(), reinterpret_cast<V *>(smem_raw), 0);
+}
+// the plain pass with the TMA store of a line-fast store side (MOA_FFT_TMA_ST)
+template <typename V, int LR>
+__global__ void __launch_bounds__(pass_max_threads<V, LR>(), 1) pass_kernel_st(const __grid_constant__ KArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    tile_body<V, LR, false, false, true>(a, int64_t(blockIdx.x) * a.W, reinterpret_cast<V *>(smem_raw), 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1877,6 +1939,41 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
+// Tensor map of a line-fast STORE side (digit 0 = adjacent lines, unit
+// stride): dims (2 digit-0 reals, the R points at out_kstr, line digits 1..),
+// boxes of W lines x min(R, 256) points (false: not expressible).
+bool set_lf_store_map(KArgs &a, const moa_pass_desc_t &d, int esize) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc || !d.lf_store || d.ndig < 1 || d.ndig > 4 || d.out_str[0] != 1 || d.out_ksplit < d.logR) return false;
+    const int64_t R = int64_t(1) << d.logR, W = d.W;
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    int rank = 0;
+    dims[rank] = cuuint64_t(2 * d.ext[0]);
+    box[rank++] = cuuint32_t(2 * W);
+    const int64_t bp = R < 256 ? R : 256;
+    dims[rank] = cuuint64_t(R);
+    strides[rank - 1] = cuuint64_t(d.out_kstr * esize);
+    box[rank++] = cuuint32_t(bp);
+    for (int i = 1; i < d.ndig; i++) {
+        dims[rank] = cuuint64_t(d.ext[i]);
+        strides[rank - 1] = cuuint64_t(d.out_str[i] * esize);
+        box[rank++] = 1;
+    }
+    if (2 * W > 256 || (W * esize) % 16 || d.ext[0] % W) return false;
+    for (int i = 0; i < rank - 1; i++)
+        if (strides[i] % 16 || strides[i] >= (cuuint64_t(1) << 40)) return false;
+    CUresult r = enc(&a.st_tmap, esize == 16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     cuuint32_t(rank), a.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    a.st_rank = rank;
+    a.st_nbox = int32_t(R / bp);
+    a.st_box_pts = int32_t(bp);
+    a.pf_ext0 = int32_t(d.ext[0]);
+    return true;
+}
+
 // Tensor map of a line-fast load side (digit 0 = adjacent lines, unit stride):
 // dims (2 digit-0 reals, the R points at in_kstr, line digits 1..), boxes of
 // W lines x min(R, 256) points.
@@ -2114,6 +2211,28 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
         cudaError_t e = std::is_same<V, double2>::value ? launch_ws<V>(kWs128, d, a, tiles, tb, stream, mods)
                                                         : launch_ws<V>(kWs64, d, a, tiles, tb, stream, mods);
         if (e != cudaErrorNotSupported) return e;
+    }
+    // TMA store (pass_kernel_st): complex128 512- / 1024-point passes with
+    // contiguous loads and a line-fast (transposed) store side.  Default where
+    // the stores are >= 8 MiB apart (cfg5's rotating 3-D passes, 16 MiB: 5.90
+    // -> 5.73 ms per pass same-box); cfg3's last pass (4 MiB apart) measured
+    // neutral (1.56 vs 1.58 ms), so it keeps the plain stores
+    // (profiles/r7b_ab.jsonl).  MOA_FFT_TMA_ST=1 forces it on every eligible
+    // pass, =0 off.
+    if constexpr (std::is_same<V, double2>::value) {
+        const char *te = std::getenv("MOA_FFT_TMA_ST");
+        const bool tma_st = te ? te[0] == '1' : d.out_kstr * int64_t(sizeof(double2)) >= (int64_t(8) << 20);
+        if (tma_st && (d.logR == 9 || d.logR == 10) && d.kind == 0 && !d.ring && !mods.npeers && !d.lf_load &&
+            d.lf_store && d.W >= 1 && set_lf_store_map(a, d, int(sizeof(double2)))) {
+            KFn<V> fs = d.logR == 9 ? &pass_kernel_st<double2, 9> : &pass_kernel_st<double2, 10>;
+            if (d.smem_bytes > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
+                if (e != cudaSuccess) return e;
+            }
+            if (pf > 0) set_prefetch(a, reinterpret_cast<const void *>(fs), d.threads, d.smem_bytes, tiles, pf);
+            fs<<<dim3(unsigned(tiles)), dim3(unsigned(d.threads)), size_t(d.smem_bytes), stream>>>(a);
+            return cudaGetLastError();
+        }
     }
     KFn<V> fn = tab[d.logR];
     if (mods.npeers || d.ring) {  // the peer-store / ring paths live in the full instantiations

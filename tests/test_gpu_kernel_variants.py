@@ -126,3 +126,60 @@ def test_small_kernel_vs_oracle_and_plain(m, torch_cuda, monkeypatch, dtype, t, 
     monkeypatch.setenv("MOA_FFT_SMALL", "0")
     y0 = run(torch_cuda, m.FFTPlan(n, batch, dtype), x)
     assert rel_l2(y.astype(np.complex128), y0.astype(np.complex128)) <= TOL[dtype]
+
+
+# TMA store of the transposed side (MOA_FFT_TMA_ST=1, pass_kernel_st): the
+# complex128 512- / 1024-point passes with contiguous loads and line-fast
+# stores (1-D last passes, every 3-D rotating pass) stage the tile in shared
+# memory and write it with tensor-map boxes.  Same arithmetic, so bit for bit
+# against the plain stores; and against the oracle.
+TMA_ST_1D = [(1 << 20, 1, None), (1 << 19, 4, None), (1 << 18, 2, None), (1 << 20, 2, [1024, 1024]),
+             (1 << 22, 1, [512, 1024, 8])]
+TMA_ST_3D = [(64, 64, 1024), (16, 512, 1024), (8, 1024, 512)]
+
+
+@pytest.mark.parametrize("n,batch,radices", TMA_ST_1D)
+def test_tma_store_1d(m, torch_cuda, monkeypatch, n, batch, radices):
+    x = synth.fill(n * batch, 41, synth.NORMAL, "c128")
+    mk = (lambda: m.FFTPlan(n, batch, "c128", radices=radices)) if radices else (lambda: m.FFTPlan(n, batch, "c128"))
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "0")
+    y0 = run(torch_cuda, mk(), x)
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "1")
+    y1 = run(torch_cuda, mk(), x)
+    assert np.array_equal(y0, y1)
+    ref = oracle.fft_radix2_rows(x, n)
+    assert rel_l2(y1, ref) <= TOL["c128"]
+    yi = run(torch_cuda, m.FFTPlan(n, batch, "c128", inverse=True, normalize=True), x)
+    refi = oracle.fft_radix2_rows_sign(x, n, +1) / n
+    assert rel_l2(yi, refi) <= TOL["c128"]
+
+
+@pytest.mark.parametrize("shape", TMA_ST_3D)
+def test_tma_store_3d(m, torch_cuda, monkeypatch, shape):
+    N = shape[0] * shape[1] * shape[2]
+    x = synth.fill(N, 43, synth.NORMAL, "c128")
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "0")
+    y0 = run(torch_cuda, m.FFTPlan.plan_3d(*shape, dtype="c128"), x)
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "1")
+    y1 = run(torch_cuda, m.FFTPlan.plan_3d(*shape, dtype="c128"), x)
+    assert np.array_equal(y0, y1)
+    ref = oracle.fft3d(x.reshape(shape)).reshape(-1)
+    assert rel_l2(y1, ref) <= TOL["c128"]
+
+
+@pytest.mark.parametrize("wname", ["cfg3", "cfg5"])
+def test_tma_store_full_size_bit_exact(m, torch_cuda, monkeypatch, wname):
+    # BASELINE.json cfg3 (2^28) / cfg5 (1024^3) at full size, on the device:
+    # the TMA-store plan bit for bit against the plain-store plan (the plain
+    # plan's whole-vector parity against the oracle is tests/test_gpu_parity.py)
+    torch = torch_cuda
+    c = synth.CONFIGS[wname]
+    x = torch.from_numpy(synth.config_input(wname)).cuda()
+    mk = (lambda: m.FFTPlan.plan_3d(*c["shape"], dtype="c128")) if wname == "cfg5" else \
+        (lambda: m.FFTPlan(c["n"], 1, "c128"))
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "0")
+    y0 = mk().exec(x)
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "1")
+    y1 = mk().exec(x)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(y0), torch.view_as_real(y1))
