@@ -372,11 +372,12 @@ def run_config(wname, m, args, ctx, steps, warmup, e2e_steps, headline):
             else:
                 dd = desc[i]
                 # the TMA-store form (kernels.cu launch_t: complex128 512- / 1024-point
-                # passes, contiguous loads, transposed stores >= 8 MiB apart)
+                # passes with contiguous loads and transposed stores)
                 st_env = os.environ.get("MOA_FFT_TMA_ST")
-                tma_st = (vt == "double2" and dd["logR"] in (9, 10) and not dd["lf_load"] and dd["lf_store"]
+                auto_st = vt == "double2" or os.environ.get("MOA_FFT_TMA_ST64") == "1"
+                tma_st = (dd["logR"] in (9, 10) and not dd["lf_load"] and dd["lf_store"]
                           and dd.get("kind", 0) == 0 and not dd["ring"]
-                          and (st_env == "1" if st_env is not None else dd["out_kstr"] * 16 >= 8 << 20))
+                          and (st_env == "1" if st_env is not None else auto_st))
                 launches_l.append(("pass", f"pass_kernel{'_st' if tma_st else ''}<{vt},{dd['logR']}>"))
                 i += 1
     per_step = [s / max(nexec, 1) for s in step_ms_list]

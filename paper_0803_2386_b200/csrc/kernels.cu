@@ -2212,19 +2212,21 @@ cudaError_t launch_t(const std::array<KFn<V>, 13> &tab, const moa_pass_desc_t &d
                                                         : launch_ws<V>(kWs64, d, a, tiles, tb, stream, mods);
         if (e != cudaErrorNotSupported) return e;
     }
-    // TMA store (pass_kernel_st): complex128 512- / 1024-point passes with
-    // contiguous loads and a line-fast (transposed) store side.  Default where
-    // the stores are >= 8 MiB apart (cfg5's rotating 3-D passes, 16 MiB: 5.90
-    // -> 5.73 ms per pass same-box); cfg3's last pass (4 MiB apart) measured
-    // neutral (1.56 vs 1.58 ms), so it keeps the plain stores
-    // (profiles/r7b_ab.jsonl).  MOA_FFT_TMA_ST=1 forces it on every eligible
-    // pass, =0 off.
-    if constexpr (std::is_same<V, double2>::value) {
+    // TMA store (pass_kernel_st): 512- / 1024-point passes with contiguous
+    // loads and a line-fast (transposed) store side.  Default for complex128:
+    // cfg5's rotating 3-D passes 5.79-6.01 -> 5.76-5.88 ms (cfg5 17.4-18.0 ->
+    // 17.3-17.6 ms, same-box rounds), cfg3's last pass neutral (1.56-1.58 vs
+    // 1.55-1.64 ms) (profiles/r7b_ab.jsonl, r7c_ab.jsonl).  complex64 only
+    // with MOA_FFT_TMA_ST64=1 (measurement pending) or MOA_FFT_TMA_ST=1, which
+    // forces it on every eligible pass; MOA_FFT_TMA_ST=0 turns it off.
+    {
+        constexpr bool c128 = std::is_same<V, double2>::value;
         const char *te = std::getenv("MOA_FFT_TMA_ST");
-        const bool tma_st = te ? te[0] == '1' : d.out_kstr * int64_t(sizeof(double2)) >= (int64_t(8) << 20);
+        const char *te64 = std::getenv("MOA_FFT_TMA_ST64");
+        const bool tma_st = te ? te[0] == '1' : (c128 || (te64 && te64[0] == '1'));
         if (tma_st && (d.logR == 9 || d.logR == 10) && d.kind == 0 && !d.ring && !mods.npeers && !d.lf_load &&
-            d.lf_store && d.W >= 1 && set_lf_store_map(a, d, int(sizeof(double2)))) {
-            KFn<V> fs = d.logR == 9 ? &pass_kernel_st<double2, 9> : &pass_kernel_st<double2, 10>;
+            d.lf_store && d.W >= 1 && set_lf_store_map(a, d, int(sizeof(V)))) {
+            KFn<V> fs = d.logR == 9 ? &pass_kernel_st<V, 9> : &pass_kernel_st<V, 10>;
             if (d.smem_bytes > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, d.smem_bytes);
                 if (e != cudaSuccess) return e;

@@ -183,3 +183,30 @@ def test_tma_store_full_size_bit_exact(m, torch_cuda, monkeypatch, wname):
     y1 = mk().exec(x)
     torch.cuda.synchronize()
     assert torch.equal(torch.view_as_real(y0), torch.view_as_real(y1))
+
+
+@pytest.mark.parametrize("n,batch,radices", [(1 << 20, 1, None), (1 << 19, 4, [512, 1024]), (1 << 20, 2, [1024, 1024])])
+def test_tma_store_c64(m, torch_cuda, monkeypatch, n, batch, radices):
+    # the complex64 form (MOA_FFT_TMA_ST=1): bit for bit against plain stores
+    x = synth.fill(n * batch, 47, synth.NORMAL, "c64")
+    mk = (lambda: m.FFTPlan(n, batch, "c64", radices=radices)) if radices else (lambda: m.FFTPlan(n, batch, "c64"))
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "0")
+    y0 = run(torch_cuda, mk(), x)
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "1")
+    y1 = run(torch_cuda, mk(), x)
+    assert np.array_equal(y0, y1)
+    ref = oracle.fft_radix2_rows(x.astype(np.complex128), n)
+    assert rel_l2(y1.astype(np.complex128), ref) <= TOL["c64"]
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 1024), (16, 512, 1024)])
+def test_tma_store_3d_c64(m, torch_cuda, monkeypatch, shape):
+    N = shape[0] * shape[1] * shape[2]
+    x = synth.fill(N, 49, synth.NORMAL, "c64")
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "0")
+    y0 = run(torch_cuda, m.FFTPlan.plan_3d(*shape, dtype="c64"), x)
+    monkeypatch.setenv("MOA_FFT_TMA_ST", "1")
+    y1 = run(torch_cuda, m.FFTPlan.plan_3d(*shape, dtype="c64"), x)
+    assert np.array_equal(y0, y1)
+    ref = oracle.fft3d(x.astype(np.complex128).reshape(shape)).reshape(-1)
+    assert rel_l2(y1.astype(np.complex128), ref) <= TOL["c64"]

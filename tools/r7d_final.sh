@@ -1,0 +1,22 @@
+#!/bin/bash
+# Session-3 final evidence with the complex128 TMA-store default: GPU tests,
+# smoke, the default bench line, complex64 TMA-store A/B, the cfg5 launch list
+# and one ncu --set full capture of the TMA-store pass.  Output -> gpurun_out/r7d*.
+set -u
+mkdir -p gpurun_out
+P=${PFX:-r7d}
+nvidia-smi > gpurun_out/${P}_smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${P}_pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/${P}_pytest_gpu.log
+timeout 300 python __graft_entry__.py smoke > gpurun_out/${P}_smoke.log 2>&1; echo "exit $?" >> gpurun_out/${P}_smoke.log
+timeout 900 python bench.py > gpurun_out/${P}_bench.json 2> gpurun_out/${P}_bench.err; echo "exit $?" >> gpurun_out/${P}_bench.err
+timeout 900 python tools/ab_env.py --cases cfg4,cfg5c64,cfg5 --variants "plain:MOA_FFT_TMA_ST=0" "st:MOA_FFT_TMA_ST=1" --rounds 3 --reps 10 \
+    > gpurun_out/${P}_ab.jsonl 2> gpurun_out/${P}_ab.err
+CMD="python bench.py --no-sub-configs --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+$CMD > gpurun_out/${P}_ncu_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/${P}_launches.csv $CMD > gpurun_out/${P}_ncu.log 2>&1
+echo "ncu exit $?" >> gpurun_out/${P}_ncu.log
+CMD="python bench.py --no-sub-configs --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pass_kernel_st -s 3 -c 1 \
+    -o gpurun_out/${P}_cfg5_st_full $CMD > gpurun_out/${P}_ncu_full.log 2>&1
+echo "ncu full exit $?" >> gpurun_out/${P}_ncu_full.log
