@@ -20,3 +20,12 @@ CMD="python bench.py --no-sub-configs --steps 1 --warmup 3 --e2e-steps 0 --no-cp
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:pass_kernel_st -s 3 -c 1 \
     -o gpurun_out/${P}_cfg5_st_full $CMD > gpurun_out/${P}_ncu_full.log 2>&1
 echo "ncu full exit $?" >> gpurun_out/${P}_ncu_full.log
+# the report itself is too large to bring back: its summary and raw page only
+python tools/summarize_ncu.py full gpurun_out/${P}_cfg5_st_full.ncu-rep > gpurun_out/${P}_cfg5_st_ncu_full.txt 2>&1
+ncu -i gpurun_out/${P}_cfg5_st_full.ncu-rep --page raw --csv 2>/dev/null | python -c "
+import csv,sys
+r=list(csv.reader(sys.stdin)); h=r[0]
+keep=[i for i,n in enumerate(h) if n.startswith(('dram__bytes','gpu__time_duration','sm__throughput','dram__throughput','launch__','smsp__warps_active'))]
+for row in r[2:]: print({h[i]: row[i] for i in keep})
+" > gpurun_out/${P}_cfg5_st_raw.txt 2>&1
+rm -f gpurun_out/${P}_cfg5_st_full.ncu-rep
