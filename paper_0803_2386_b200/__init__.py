@@ -257,13 +257,33 @@ def moa_fft_launches_per_exec(plan: int) -> int:
     return int(lib.moa_fft_launches_per_exec(plan))
 
 
+def _default_nccl_lib() -> None:
+    # Point the C side at the NCCL wheel next to torch (2.28: has ncclAlltoAll)
+    # unless the caller chose one; without it the C side falls back to the
+    # search path and, on an older NCCL, to grouped ncclSend / ncclRecv.
+    if os.environ.get("MOA_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for d in (spec.submodule_search_locations if spec else []):
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["MOA_NCCL_LIB"] = cand
+            return
+
+
 def moa_fft_get_unique_id() -> bytes:
+    _default_nccl_lib()
     buf = (ctypes.c_uint8 * 128)()
     _check(lib.moa_fft_get_unique_id(buf))
     return bytes(buf)
 
 
 def moa_fft_dist_init(rank: int, ngpu: int, uid: bytes) -> None:
+    _default_nccl_lib()
     buf = (ctypes.c_uint8 * 128)(*uid)
     _check(lib.moa_fft_dist_init(rank, ngpu, buf))
 

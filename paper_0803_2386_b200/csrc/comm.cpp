@@ -34,7 +34,11 @@ struct Nccl {
     decltype(&::ncclCommInitRank) commInitRank = nullptr;
     decltype(&::ncclCommDestroy) commDestroy = nullptr;
     decltype(&::ncclCommAbort) commAbort = nullptr;
-    decltype(&::ncclAlltoAll) alltoAll = nullptr;
+    decltype(&::ncclAlltoAll) alltoAll = nullptr;  // NCCL >= 2.28; else grouped send / recv below
+    decltype(&::ncclSend) send = nullptr;
+    decltype(&::ncclRecv) recv = nullptr;
+    decltype(&::ncclGroupStart) groupStart = nullptr;
+    decltype(&::ncclGroupEnd) groupEnd = nullptr;
     decltype(&::ncclAllGather) allGather = nullptr;
     decltype(&::ncclAllReduce) allReduce = nullptr;
     decltype(&::ncclGetErrorString) errStr = nullptr;
@@ -44,25 +48,69 @@ ncclComm_t g_comm = nullptr;
 int g_rank = -1, g_ngpu = 0;
 bool g_loopback = false;
 
+// Binds one candidate library; false (nothing kept) when it lacks an entry point
+// the path needs.  The all-to-all is ncclAlltoAll where the library has it
+// (NCCL >= 2.28), else one ncclSend + ncclRecv per peer inside a group.
+bool bind_nccl(void *h, bool need_alltoall) {
+    Nccl n;
+    n.h = h;
+    n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+    n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+    n.commAbort = (decltype(n.commAbort))dlsym(h, "ncclCommAbort");
+    n.alltoAll = (decltype(n.alltoAll))dlsym(h, "ncclAlltoAll");
+    n.send = (decltype(n.send))dlsym(h, "ncclSend");
+    n.recv = (decltype(n.recv))dlsym(h, "ncclRecv");
+    n.groupStart = (decltype(n.groupStart))dlsym(h, "ncclGroupStart");
+    n.groupEnd = (decltype(n.groupEnd))dlsym(h, "ncclGroupEnd");
+    n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+    n.allReduce = (decltype(n.allReduce))dlsym(h, "ncclAllReduce");
+    n.errStr = (decltype(n.errStr))dlsym(h, "ncclGetErrorString");
+    if (!n.getUniqueId || !n.commInitRank || !n.commDestroy || !n.allGather || !n.allReduce) return false;
+    const bool p2p = n.send && n.recv && n.groupStart && n.groupEnd;
+    if (need_alltoall ? !n.alltoAll : !(n.alltoAll || p2p)) return false;
+    g_nccl = n;
+    return true;
+}
+
 moa_status_t load_nccl() {
     if (g_nccl.h) return MOA_OK;
-    const char *cand[] = {std::getenv("MOA_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
-    void *h = nullptr;
-    for (const char *c : cand)
-        if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
-    if (!h) return fail(MOA_ENCCL, "NCCL: cannot dlopen libnccl.so.2 (set MOA_NCCL_LIB)");
-    g_nccl.h = h;
-    g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
-    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
-    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
-    g_nccl.commAbort = (decltype(g_nccl.commAbort))dlsym(h, "ncclCommAbort");
-    g_nccl.alltoAll = (decltype(g_nccl.alltoAll))dlsym(h, "ncclAlltoAll");
-    g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
-    g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
-    g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
-    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.commDestroy || !g_nccl.alltoAll)
-        return fail(MOA_ENCCL, "NCCL: the loaded library lacks ncclAlltoAll (needs NCCL >= 2.28)");
-    return MOA_OK;
+    // MOA_NCCL_LIB, then a libnccl this process has already loaded (torch's
+    // bundled one), then the search path.  First round: a library with
+    // ncclAlltoAll; second: any with send / recv (the system 2.27).
+    const char *env = std::getenv("MOA_NCCL_LIB");
+    bool opened = false;
+    for (int round = 0; round < 2; round++) {
+        struct { const char *name; int flags; } cand[] = {
+            {env, RTLD_NOW | RTLD_GLOBAL},
+            {"libnccl.so.2", RTLD_NOW | RTLD_NOLOAD},
+            {"libnccl.so.2", RTLD_NOW | RTLD_GLOBAL},
+            {"libnccl.so", RTLD_NOW | RTLD_GLOBAL}};
+        for (auto &c : cand) {
+            if (!c.name || !c.name[0]) continue;
+            void *h = dlopen(c.name, c.flags);
+            if (!h) continue;
+            opened = true;
+            if (bind_nccl(h, round == 0)) return MOA_OK;
+            dlclose(h);
+        }
+    }
+    return fail(MOA_ENCCL, opened ? "NCCL: the loaded library lacks ncclAlltoAll and ncclSend / ncclRecv"
+                                  : "NCCL: cannot dlopen libnccl.so.2 (set MOA_NCCL_LIB)");
+}
+
+// chunk h (cnt elements) of `src` to rank h, chunk g of `dst` from rank g
+ncclResult_t nccl_all_to_all(const void *src, void *dst, size_t cnt, ncclDataType_t ty, size_t tsize, int p,
+                             cudaStream_t s) {
+    if (g_nccl.alltoAll) return g_nccl.alltoAll(src, dst, cnt, ty, g_comm, s);
+    ncclResult_t r = g_nccl.groupStart();
+    if (r != ncclSuccess) return r;
+    for (int h = 0; h < p && r == ncclSuccess; h++) {
+        r = g_nccl.send(static_cast<const char *>(src) + size_t(h) * cnt * tsize, cnt, ty, h, g_comm, s);
+        if (r == ncclSuccess) r = g_nccl.recv(static_cast<char *>(dst) + size_t(h) * cnt * tsize, cnt, ty, h, g_comm, s);
+    }
+    ncclResult_t e = g_nccl.groupEnd();
+    return r != ncclSuccess ? r : e;
 }
 
 moa_status_t nccl_fail(ncclResult_t r, const char *what) {
@@ -467,8 +515,9 @@ moa_status_t dist_exec(const std::vector<DistRank> &ranks, DistBackend be, moa_d
             // loopback: every virtual rank's kernels run in order on one stream
         } else if (be == DistBackend::Nccl) {
             const size_t cnt = size_t(st.count) * 2;
-            ncclResult_t rr = g_nccl.alltoAll(ranks[0].bufs[st.src], ranks[0].bufs[st.dst], cnt,
-                                              dtype == MOA_C128 ? ncclDouble : ncclFloat, g_comm, s);
+            ncclResult_t rr = nccl_all_to_all(ranks[0].bufs[st.src], ranks[0].bufs[st.dst], cnt,
+                                              dtype == MOA_C128 ? ncclDouble : ncclFloat,
+                                              dtype == MOA_C128 ? 8 : 4, p, s);
             if (rr != ncclSuccess) return nccl_fail(rr, "all-to-all");
         } else {  // loopback all-to-all: chunk h of rank g -> chunk g of rank h (one copy per chunk)
             const size_t cb = size_t(st.count) * dp0->esize;
