@@ -201,6 +201,10 @@ moa_status_t moa_fft_prof_end(moa_fft_plan_t plan, double *step_ms, int max_step
  *   moa_fft_dist_init     : every rank, with the same id, before planning with
  *                           ngpu > 1; binds the communicator to the current device.
  *   moa_fft_dist_finalize : destroy the communicator.
+ * libnccl is bound at the first of these calls: $MOA_NCCL_LIB, else a libnccl
+ * the process already holds, else the loader's search path; the exchanges use
+ * ncclAlltoAll where the library has it (NCCL >= 2.28), else one ncclSend +
+ * ncclRecv per peer in a group.  MOA_ENCCL if no usable library is found.
  */
 moa_status_t moa_fft_get_unique_id(uint8_t id[128]);
 moa_status_t moa_fft_dist_init(int rank, int ngpu, const uint8_t id[128]);
